@@ -1,0 +1,341 @@
+"""Benchmark: B0 -> J/psi K pi phase-space generation + weight integration
+(BASELINE.json configs[1]: 1e8 events per B200), plus the FCN (configs[3]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = generate EVENTS_PER_GPU events per GPU into HBM (13 fp64 SoA
+columns, 104 B/event), with the weight moments (sum w, sum w^2) fused into the
+same kernel, then the cross-GPU gather of the chunk partials (NCCL) and the
+deterministic fold -> weight sum / mean / variance.  Weak scaling: rank r
+generates global rows [r * EVENTS_PER_GPU, (r+1) * EVENTS_PER_GPU).
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference
+algorithm's CPU implementation (the bit-exact C oracle port, all host
+threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "phase-space events/s (B0→J/ψKπ, fp64) and FCN evals/s @1e7 evts, 1–8 B200"
+M_B0, DAUGHTERS = 5.27966, (3.0969, 0.493677, 0.13957039)
+EVENTS_PER_GPU = 100_000_000
+BYTES_PER_EVENT = 8 * (4 * 3 + 1)          # algorithmic HBM bytes written per 3-body event
+FCN_EVENTS = 10_000_000
+
+
+def _peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json copy BW)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _traffic() -> float | None:
+    """dram read+write bytes per launch of the generator, from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "generate_traffic.json")) as fh:
+            return float(json.load(fh)["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit()),
+                "samples": len(rows), "reasons": reasons}
+
+
+def cpu_reference(steps: int, warmup: int, sample: int | None = None) -> dict:
+    """The reference algorithm on the host cores: bit-exact C port of
+    phsp_generate + numpy weight integration, all threads."""
+    import numpy as np
+
+    from oracle import oracle as O  # the CPU baseline leg (test/bench infrastructure only)
+
+    threads = os.cpu_count() or 1
+    if sample is None:
+        t0 = time.perf_counter()
+        O.generate(DAUGHTERS, M_B0, 1_000_000, 1, 1, threads=threads)
+        rate = 1_000_000 / (time.perf_counter() - t0)
+        sample = int(min(max(rate * 3.0, 1_000_000), 50_000_000))   # ~3 s per step
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        cols = O.generate(DAUGHTERS, M_B0, sample, 1, 1, ev_begin=i * sample, threads=threads)
+        w = cols["weight"]
+        _ = (float(np.sum(w)), float(np.sum(w * w)))
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+        del cols, w
+    t = statistics.median(times)
+    return {"value": sample / t, "unit": "events/s", "cores": threads, "kind": "port",
+            "sample": f"{sample} B0->J/psi K pi events + weight sums per step (C oracle port, "
+                      f"-ffp-contract=off, {threads} pthreads), median of {steps}",
+            "seconds_per_step": t}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base = cpu_reference(args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "events/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": base["seconds_per_step"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: B0->J/psi K pi 3-body generation + weight integration "
+                               "(bounded CPU sample per step)", "events_per_step": None},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    line["config"]["events_per_step"] = int(round(base["value"] * base["seconds_per_step"]))
+    print(json.dumps(line), flush=True)
+
+
+def fcn_bench(hk, torch, evals: int = 200) -> dict:
+    """FCN evals/s on a 1e7-event gauss+exp data set resident in HBM (configs[3])."""
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    mean, sigma, tau = hk.Parameter("mean", 5.0), hk.Parameter("sigma", 0.5, lower=1e-4), hk.Parameter("tau", 3.0, lower=1e-4)
+    g, e = hk.shape_gaussian(mean, sigma), hk.shape_exponential(tau)
+    n_sig, n_bkg = hk.Parameter("n_sig", 4e6, lower=0.0), hk.Parameter("n_bkg", 6e6, lower=0.0)
+    model = hk.add_pdfs([n_sig, n_bkg], [hk.make_pdf(g, hk.gaussian_norm(g), region),
+                                         hk.make_pdf(e, hk.exponential_norm(e), region)])
+    data = hk.generate_model_sample(model, hk.RngKey(7, 2), poisson=False)   # exactly 1e7 events, on device
+    assert len(data) == FCN_EVENTS
+    points = [(5.0, 0.5, 3.0), (4.9, 0.55, 2.8)]
+    for i in range(5):
+        mean.set(points[i % 2][0]); sigma.set(points[i % 2][1]); tau.set(points[i % 2][2])
+        hk.nll(model, data, ["x0"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(evals):
+        p = points[i % 2]
+        mean.set(p[0]); sigma.set(p[1]); tau.set(p[2])     # forces host norm recomputation
+        hk.nll(model, data, ["x0"])
+    dt = (time.perf_counter() - t0) / evals
+    # device-only time of the FCN kernels
+    from paper_1711_05683_b200 import _lib
+    from paper_1711_05683_b200.fitting import lower_model
+    x = data.device_column("x0")
+    lm = lower_model(model)
+    parts = _lib.empty(_lib.num_chunks(FCN_EVENTS))
+    bad = _lib.bad_cells(1)
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        _lib.lib().hk_nll_partials(_lib.ptr(x), FCN_EVENTS, lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+    ev0.record(st)
+    for _ in range(evals):
+        _lib.lib().hk_nll_partials(_lib.ptr(x), FCN_EVENTS, lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+    ev1.record(st)
+    ev1.synchronize()
+    kt = ev0.elapsed_time(ev1) / evals * 1e-3
+    return {"metric": "FCN evals/s @1e7 events (gauss+exp extended NLL, fp64)", "value": 1.0 / dt,
+            "unit": "evals/s", "us_per_eval": dt * 1e6, "kernel_us_per_eval": kt * 1e6,
+            "kernel_events_per_s": FCN_EVENTS / kt, "evals": evals,
+            "data": "1e7 events from generate_model_sample(build_model(scale=200), RngKey(7,2), poisson=False) on device"}
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    import paper_1711_05683_b200 as hk
+    from paper_1711_05683_b200 import _lib
+    from paper_1711_05683_b200.parallel import gather_partials
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
+    n = EVENTS_PER_GPU
+    n_total = n * world
+    key = hk.RngKey(1, 1)
+    d = _lib.make_decay(spec, mother, M_B0)
+    k = _lib.make_key(key)
+    cols = [_lib.empty(n) for _ in range(13)]
+    colp = _lib.ptr_array(cols)
+    wpart = _lib.empty(2 * _lib.num_chunks(n))
+    st = torch.cuda.current_stream()
+    L = _lib.lib()
+
+    def step(gen_events=None):
+        if gen_events:
+            gen_events[0].record(st)
+        _lib.check(L.hk_phsp_generate(d, k, rank * n, n, colp, _lib.ptr(wpart), st.cuda_stream), "generate")
+        if gen_events:
+            gen_events[1].record(st)
+        full = gather_partials(wpart, n_total, 2)
+        return _lib.fold(full, _lib.num_chunks(n_total), 2)
+
+    for _ in range(args.warmup):
+        tot = step()
+    torch.cuda.synchronize()
+    gen_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t0.record(st)
+        for i in range(args.steps):
+            tot = step(gen_ev[i])
+        t1.record(st)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed = t0.elapsed_time(t1) * 1e-3
+    gen_times = [a.elapsed_time(b) * 1e-3 for a, b in gen_ev]
+    if dist:
+        tt = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    sums = tot.cpu().numpy()
+    per_step = elapsed / args.steps
+    value = n_total / per_step
+    gen_avg = sum(gen_times) / len(gen_times)
+    peaks = _peaks()
+    achieved = BYTES_PER_EVENT * n / gen_avg / 1e9
+    traffic = _traffic()
+
+    # end to end through the public API, host buffers (pinned), D2H inside the timed region
+    e2e = None
+    if rank == 0 or world > 1:
+        del cols
+        torch.cuda.empty_cache()
+        host = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in range(13)]
+        hk.phsp_generate_to_host(spec, mother, n, key, row_offset=rank * n, out=host)   # warm (staging alloc)
+        e_steps = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        a0 = time.perf_counter()
+        for _ in range(e_steps):
+            _, ws = hk.phsp_generate_to_host(spec, mother, n, key, row_offset=rank * n, out=host)
+        e_dt = (time.perf_counter() - a0) / e_steps
+        e2e = {"value": n_total / e_dt if world == 1 else None, "per_gpu_value": n / e_dt, "unit": "events/s",
+               "h2d_bytes_per_step": ctypes.sizeof(_lib.hk_decay_t) + ctypes.sizeof(_lib.hk_key_t),
+               "d2h_bytes_per_step": BYTES_PER_EVENT * n + 16,
+               "api": "phsp_generate_to_host (pinned host columns; generation overlapped with D2H)",
+               "steps": e_steps}
+        if dist:
+            tt = torch.tensor([e_dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e["value"] = n_total / float(tt.item())
+        del host
+
+    fcn = None
+    if rank == 0 and not args.no_fcn:
+        fcn = fcn_bench(hk, torch, evals=args.fcn_evals)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(steps=1, warmup=0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: B0->J/psi K pi 3-body phase-space generation + weight integration "
+                                   "(sum/mean/variance), 1e8 events per GPU, stored to HBM",
+                       "events_per_gpu": n, "events_per_step": n_total, "rng": "reference SplitMix64 stream",
+                       "parallelism": f"dp{world} (contiguous event shards, NCCL gather of chunk partials)",
+                       "l2": "each step writes 10.4 GB per GPU (> 126 MB L2): no flush needed",
+                       "weight_sum": float(sums[0]), "weight_mean": float(sums[0] / n_total),
+                       "weight_variance": float(max(sums[1] / n_total - (sums[0] / n_total) ** 2, 0.0))},
+            "roofline": {"bound": "hbm", "kernel": "k_generate<3, reference>", "achieved": achieved,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "peak_source": peaks["source"], "traffic": traffic,
+                         "algorithmic_bytes_per_event": BYTES_PER_EVENT,
+                         "kernel_ms": gen_avg * 1e3, "kernel_share_of_step": gen_avg / per_step},
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "cpu_baseline": cpu,
+            "fcn": fcn,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-fcn", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fcn-evals", type=int, default=200)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

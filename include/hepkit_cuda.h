@@ -1,0 +1,260 @@
+/*
+ * hepkit_cuda.h -- C ABI of libhepkit_cuda.so, the B200 (sm_100a) hot path of
+ * the reference's event-parallel map/reduce (arXiv:1711.05683 -> `hepkit`).
+ *
+ * The reference has no FFI: its seam is the public Python API whose bodies all
+ * go through parallel.run_batches (parallel.py:56-71).  Each entry point below
+ * replaces the *body* of one such function; the Python package
+ * paper_1711_05683_b200 keeps the reference names/signatures/exceptions and
+ * calls these through ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - plain C types only; every array argument is a raw pointer + a size;
+ *    "d_" pointers are device (HBM) addresses, "h_" pointers host addresses;
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *  - calls are asynchronous on `stream` unless documented otherwise;
+ *  - return value: HK_OK (0) or an HK_E* code; hk_last_error() gives text.
+ *  - event ("row") indices are 64-bit and global: row r of a run draws the RNG
+ *    counters (r + key.counter) * D + j (phasespace.py:105-109), so any window
+ *    [ev_begin, ev_begin + ev_count) -- a GPU shard, say -- is bit-identical to
+ *    the same rows of a one-shot run.
+ *  - reductions produce one partial per HK_CHUNK rows (parallel.py:18) in a
+ *    fixed in-block tree order, then hk_fold_partials folds them in a fixed
+ *    tree; results are deterministic and independent of the launch grid.
+ */
+#ifndef HEPKIT_CUDA_H
+#define HEPKIT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HK_ABI_VERSION 1
+
+/* status codes */
+#define HK_OK 0
+#define HK_EINVAL 1       /* bad argument (sizes, pointers, arity) */
+#define HK_ECUDA 2        /* CUDA runtime error (see hk_last_error) */
+#define HK_EDOMAIN 3      /* per-event domain failure; first bad row reported */
+#define HK_EUNSUPPORTED 4 /* configuration outside the compiled kernels */
+
+#define HK_CHUNK 4096        /* rows per reduction partial (parallel.py:18) */
+#define HK_MAX_DAUGHTERS 16  /* templated fast path covers n <= 8 */
+#define HK_MAX_PROGRAM 48    /* ops per device functor program */
+#define HK_MAX_SLOTS 16      /* virtual registers per program */
+#define HK_MAX_COMPONENTS 8  /* p.d.f. components per extended model */
+#define HK_NO_BAD_ROW UINT64_MAX
+
+/* RNG selection: the reference SplitMix64 stream (rng.py:98-125), bit-exact,
+ * or the production Philox4x32-10 stream (SPEC.md:343 allows any
+ * counter-based bijection). */
+#define HK_RNG_REFERENCE 0
+#define HK_RNG_PHILOX 1
+
+/* RngKey (rng.py:45-62); all fields already reduced mod 2^64 (rng.py:105). */
+typedef struct hk_key {
+  uint64_t seed;
+  uint64_t stream;
+  uint64_t counter;
+  int32_t mode; /* HK_RNG_* */
+  int32_t _pad;
+} hk_key_t;
+
+/* DecaySpec (phasespace.py:36-57) plus the mother four-vector of
+ * phsp_generate (phasespace.py:162-188).  T and csum are computed on the host
+ * with numpy (phasespace.py:94-97) so their rounding is the reference's. */
+typedef struct hk_decay {
+  int32_t n;      /* daughters, 2..HK_MAX_DAUGHTERS */
+  int32_t moving; /* boost every daughter by the mother (phasespace.py:181) */
+  double mother_mass;
+  double T;
+  double masses[HK_MAX_DAUGHTERS];
+  double csum[HK_MAX_DAUGHTERS];
+  double mother[4]; /* e, px, py, pz */
+  double m_mother;  /* invariant_mass(mother) (phasespace.py:175) */
+} hk_decay_t;
+
+/* Device functor program: an SSA register program lowered on the host from a
+ * FunctorExpr tree (functors.py:79-249) composed with a traced arg_builder.
+ * Each op writes slot dst[i] from slots a[i], b[i]. */
+enum hk_opcode {
+  HK_OP_COL = 0,    /* dst = column[a]  (0 = weight, 1 + 4(j-1) + c = p_j comp c) */
+  HK_OP_CONST = 1,  /* dst = cst[i] */
+  HK_OP_ADD = 2,    /* dst = a + b */
+  HK_OP_SUB = 3,    /* dst = a - b */
+  HK_OP_MUL = 4,    /* dst = a * b */
+  HK_OP_DIV = 5,    /* dst = a / b; b == 0 is a domain error (functors.py:200-207) */
+  HK_OP_NEG = 6,    /* dst = -a */
+  HK_OP_SQRT = 7,   /* dst = sqrt(a) */
+  HK_OP_EXP = 8,    /* dst = exp(a) */
+  HK_OP_LOG = 9,    /* dst = log(a) */
+  HK_OP_GAUSS = 10, /* dst = exp(-0.5 z z)/(s sqrt(2pi)), z=(a-cst[i])/cst2[i] (functors.py:137-143) */
+  HK_OP_EXPO = 11,  /* dst = exp(-a / cst[i]) (functors.py:157-161) */
+  HK_OP_BW = 12,    /* dst = 1/((a - m0^2)^2 + m0^2 g0^2), m0=cst[i], g0=cst2[i] */
+  HK_OP_ADD0 = 13,  /* dst = a + 0.0 (Coordinate, functors.py:248-249) */
+  HK_OP_SQUARE = 14 /* dst = a * a */
+};
+
+typedef struct hk_program {
+  int32_t n_ops;
+  int32_t result; /* slot holding the value */
+  int32_t op[HK_MAX_PROGRAM];
+  int32_t dst[HK_MAX_PROGRAM];
+  int32_t a[HK_MAX_PROGRAM];
+  int32_t b[HK_MAX_PROGRAM];
+  double cst[HK_MAX_PROGRAM];
+  double cst2[HK_MAX_PROGRAM];
+} hk_program_t;
+
+/* ExtendedModel (fitting.py:126-166) lowered for the FCN: per component the
+ * yield N_k (a Parameter value), the host-computed norm_k (fitting.py:80-89)
+ * and the shape kind/parameters. */
+#define HK_SHAPE_GAUSS 0 /* p0 = mean, p1 = sigma */
+#define HK_SHAPE_EXPO 1  /* p0 = tau */
+typedef struct hk_model {
+  int32_t n_comp;
+  int32_t _pad;
+  int32_t kind[HK_MAX_COMPONENTS];
+  double yield[HK_MAX_COMPONENTS];
+  double norm[HK_MAX_COMPONENTS];
+  double p0[HK_MAX_COMPONENTS];
+  double p1[HK_MAX_COMPONENTS];
+} hk_model_t;
+
+/* ---------------------------------------------------------------- runtime */
+int hk_abi_version(void);
+/* Copy the last error message of this thread into buf (NUL-terminated). */
+int hk_last_error(char* buf, size_t len);
+/* Number of CUDA devices visible; sets *sm_count to device 0's SM count. */
+int hk_device_info(int* n_devices, int* sm_count);
+/* Number of 4096-row chunk partials for ev_count rows. */
+int64_t hk_num_chunks(int64_t ev_count);
+
+/* -------------------------------------------------------------------- RNG */
+/* rng.py:115-120 raw64 / :123-125 uniform_array at key.counter + d_counters[i].
+ * Mode HK_RNG_PHILOX is not a reference stream (uniform only, for tests). */
+int hk_rng_raw64(const hk_key_t* key, const uint64_t* d_counters, int64_t n, uint64_t* d_out,
+                 void* stream);
+int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, double* d_out,
+                   void* stream);
+
+/* ------------------------------------------------------------- generation */
+/* phsp_generate (phasespace.py:162-188) for rows [ev_begin, ev_begin+ev_count):
+ * writes 4n+1 columns, d_cols[0] = weight, d_cols[1+4j+c] = daughter j+1,
+ * component c (e, px, py, pz) (phsp_schema, phasespace.py:60-64).
+ * d_wpartials (optional, NULL to skip): 2 doubles per chunk = (sum w, sum w^2),
+ * the weight-integration moments fused into the same pass. */
+int hk_phsp_generate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
+                     int64_t ev_count, double* const* d_cols, double* d_wpartials, void* stream);
+
+/* Same rows written to HOST memory (h_cols[4n+1], pinned for full speed):
+ * generation into a double-buffered device staging area (d_stage, stage_bytes)
+ * overlapped with device->host copies on a second stream.  Synchronous.
+ * h_wsums (optional): 2 doubles, folded (sum w, sum w^2). */
+int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
+                          int64_t ev_count, double* const* h_cols, double* h_wsums,
+                          void* d_stage, size_t stage_bytes, void* stream);
+
+/* phsp_decay_chain (phasespace.py:237-288), standalone on an existing block:
+ * reads parent weight d_w_in and the daughter's four columns d_p4_in[4];
+ * writes d_w_out and 4*n_sub sub-daughter columns d_sub_cols (the caller
+ * splices them into the schema).  Rows failing the mass check
+ * (phasespace.py:259-268) are reported through *d_first_bad (atomicMin;
+ * initialise to HK_NO_BAD_ROW). */
+int hk_phsp_decay_chain(const double* d_w_in, const double* const* d_p4_in,
+                        const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
+                        int64_t ev_count, double* d_w_out, double* const* d_sub_cols,
+                        uint64_t* d_first_bad, void* stream);
+
+/* Fused generate + decay_chain (config C3): parent spec/key generate, daughter
+ * `daughter_index` (1-based) decays by sub/sub_key, output in the spliced
+ * schema order (4*(n-1+n_sub)+1 columns). */
+int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t daughter_index,
+                           const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
+                           int64_t ev_count, double* const* d_cols, double* d_wpartials,
+                           uint64_t* d_first_bad, void* stream);
+
+/* --------------------------------------------------------------- averages */
+/* phsp_average moments (phasespace.py:310-329) over stored columns: per chunk
+ * 5 doubles (sum w, sum w f, sum w^2, sum w^2 f, sum w^2 f^2), f = program.
+ * Non-finite f (phasespace.py:314-316) or a zero divisor is reported via
+ * *d_first_bad. */
+int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_count,
+                    const hk_program_t* f, double* d_partials, uint64_t* d_first_bad,
+                    void* stream);
+
+/* map_evaluate (functors.py:288-318): d_out[i] = program(columns at row i).
+ * Zero divisors -> d_first_bad (may be NULL). */
+int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const hk_program_t* f,
+                   double* d_out, uint64_t* d_first_bad, void* stream);
+
+/* Fused generate -> f -> moments with no event store (config C5). */
+int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
+                      int64_t ev_count, const hk_program_t* f, double* d_partials,
+                      uint64_t* d_first_bad, void* stream);
+
+/* Deterministic fold of n_parts partials of `width` (<= 32) doubles each
+ * (parallel.py:86-92 semantics, fixed tree order) into d_out[width]. */
+int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,
+                     void* stream);
+
+/* ------------------------------------------------------------------- FCN */
+/* Extended NLL event sum (fitting.py:197-207): per chunk sum_e ln density(x_e);
+ * density <= 0 or non-finite -> *d_first_bad (fitting.py:200-205). */
+int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
+                    uint64_t* d_first_bad, void* stream);
+
+/* One FCN evaluation end to end: partials + fold + 16-byte readback.
+ * Synchronous.  *h_logsum = sum_e ln density; *h_first_bad = first failing
+ * row or HK_NO_BAD_ROW.  d_work needs hk_num_chunks(n) + 2 doubles. */
+int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
+                double* h_logsum, uint64_t* h_first_bad, void* stream);
+
+/* Yield-stationarity sums (fitting.py:401-434) for K <= 4 components: per
+ * chunk K values sum_e r_k and K*K values sum_e r_k r_j, r_k = pdf_k(x)/density(x),
+ * pdf_k = shape_k/norm_k.  Width K + K*K doubles per chunk.  density <= 0
+ * (NaN included, fitting.py:418-420) -> *d_first_bad. */
+int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
+                      uint64_t* d_first_bad, void* stream);
+
+/* density(x) for n values (the value the error message quotes). */
+int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,
+                     void* stream);
+
+/* ------------------------------------------------------------- sampling */
+/* sample_pdf (rng.py:177-242): rows [ev_begin, ev_begin+count) of an
+ * accept-reject sample of program f on the box lo + [0, span)^dim.
+ * d_bad[0]: packed (batch << 40 | round << 24 | row % 65536) of the first
+ * proposal above `ceiling` (CeilingError); d_bad[1]: first row with no
+ * acceptance in max_rounds.  Both initialised to HK_NO_BAD_ROW. */
+int hk_sample_pdf(const hk_program_t* f, int32_t dim, const double* lo, const double* span,
+                  double ceiling, const hk_key_t* key, uint64_t ev_begin, int64_t count,
+                  int32_t max_rounds, double* const* d_out, uint64_t* d_bad, void* stream);
+
+/* ----------------------------------------------------------- unweighting */
+/* phsp_unweight accept test (phasespace.py:225-227): u_i * w_max < w_i with
+ * u_i at key.counter + ev_begin + i.  Writes d_flags (uint8), per-chunk
+ * accept counts into d_counts (int64 per chunk) and reports w > w_max rows
+ * via *d_first_bad (phasespace.py:217-221). */
+int hk_unweight_flags(const double* d_w, int64_t n, double w_max, const hk_key_t* key,
+                      uint64_t ev_begin, uint8_t* d_flags, int64_t* d_counts,
+                      uint64_t* d_first_bad, void* stream);
+
+/* Order-preserving compaction of n_cols columns by d_flags given the exclusive
+ * prefix of per-chunk counts d_offsets (int64 per chunk); accepted rows of
+ * d_in[c] land in d_out[c]; weight column index `weight_col` (or -1) is set to 1.0
+ * (phasespace.py:230-234). */
+int hk_compact(const double* const* d_in, int32_t n_cols, int64_t n, const uint8_t* d_flags,
+               const int64_t* d_offsets, double* const* d_out, int32_t weight_col, void* stream);
+
+/* Exclusive scan of n int64 values (per-chunk counts) -> d_out; total -> d_total. */
+int hk_scan_counts(const int64_t* d_counts, int64_t n, int64_t* d_out, int64_t* d_total,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEPKIT_CUDA_H */

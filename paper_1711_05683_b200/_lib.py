@@ -1,0 +1,246 @@
+"""ctypes binding of libhepkit_cuda.so (include/hepkit_cuda.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every
+hot-path call raises :class:`DeviceUnavailable`.  Device memory, streams and
+(multi-GPU) collectives come from PyTorch; all arithmetic on the hot path is
+in the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhepkit_cuda.so")
+
+HK_OK, HK_EINVAL, HK_ECUDA, HK_EDOMAIN, HK_EUNSUPPORTED = 0, 1, 2, 3, 4
+HK_CHUNK = 4096
+HK_MAX_DAUGHTERS = 16
+HK_MAX_PROGRAM = 48
+HK_MAX_SLOTS = 16
+HK_MAX_COMPONENTS = 8
+HK_NO_BAD_ROW = (1 << 64) - 1
+HK_RNG_REFERENCE, HK_RNG_PHILOX = 0, 1
+HK_SHAPE_GAUSS, HK_SHAPE_EXPO = 0, 1
+
+# opcodes (enum hk_opcode)
+OP_COL, OP_CONST, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_NEG, OP_SQRT, OP_EXP, OP_LOG = range(10)
+OP_GAUSS, OP_EXPO, OP_BW, OP_ADD0, OP_SQUARE = range(10, 15)
+
+# symbols the header declares; tests check the .so exports every one
+EXPORTS = (
+    "hk_abi_version", "hk_last_error", "hk_device_info", "hk_num_chunks",
+    "hk_rng_raw64", "hk_rng_uniform",
+    "hk_phsp_generate", "hk_phsp_generate_host", "hk_phsp_decay_chain", "hk_phsp_generate_chain",
+    "hk_phsp_moments", "hk_map_program", "hk_phsp_integrate", "hk_fold_partials",
+    "hk_nll_partials", "hk_nll_eval", "hk_model_density",
+    "hk_yield_partials",
+    "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
+)
+
+
+class DeviceUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is not available (no CPU fallback)."""
+
+
+class KernelError(RuntimeError):
+    """A library call failed for a reason other than a per-event domain error."""
+
+
+class hk_key_t(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("stream", ctypes.c_uint64),
+                ("counter", ctypes.c_uint64), ("mode", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
+class hk_decay_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("moving", ctypes.c_int32),
+                ("mother_mass", ctypes.c_double), ("T", ctypes.c_double),
+                ("masses", ctypes.c_double * HK_MAX_DAUGHTERS),
+                ("csum", ctypes.c_double * HK_MAX_DAUGHTERS),
+                ("mother", ctypes.c_double * 4), ("m_mother", ctypes.c_double)]
+
+
+class hk_program_t(ctypes.Structure):
+    _fields_ = [("n_ops", ctypes.c_int32), ("result", ctypes.c_int32),
+                ("op", ctypes.c_int32 * HK_MAX_PROGRAM), ("dst", ctypes.c_int32 * HK_MAX_PROGRAM),
+                ("a", ctypes.c_int32 * HK_MAX_PROGRAM), ("b", ctypes.c_int32 * HK_MAX_PROGRAM),
+                ("cst", ctypes.c_double * HK_MAX_PROGRAM), ("cst2", ctypes.c_double * HK_MAX_PROGRAM)]
+
+
+class hk_model_t(ctypes.Structure):
+    _fields_ = [("n_comp", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("kind", ctypes.c_int32 * HK_MAX_COMPONENTS),
+                ("yield_", ctypes.c_double * HK_MAX_COMPONENTS),
+                ("norm", ctypes.c_double * HK_MAX_COMPONENTS),
+                ("p0", ctypes.c_double * HK_MAX_COMPONENTS),
+                ("p1", ctypes.c_double * HK_MAX_COMPONENTS)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_U64 = ctypes.c_uint64
+_I32 = ctypes.c_int32
+_SIGS = {
+    "hk_abi_version": (ctypes.c_int, []),
+    "hk_last_error": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t]),
+    "hk_device_info": (ctypes.c_int, [_P, _P]),
+    "hk_num_chunks": (_I64, [_I64]),
+    "hk_rng_raw64": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "hk_rng_uniform": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "hk_phsp_generate": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P]),
+    "hk_phsp_generate_host": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P, ctypes.c_size_t, _P]),
+    "hk_phsp_decay_chain": (ctypes.c_int, [_P, _P, _P, _P, _U64, _I64, _P, _P, _P, _P]),
+    "hk_phsp_generate_chain": (ctypes.c_int, [_P, _P, _I32, _P, _P, _U64, _I64, _P, _P, _P, _P]),
+    "hk_phsp_moments": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _P]),
+    "hk_phsp_integrate": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P, _P]),
+    "hk_map_program": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _P]),
+    "hk_fold_partials": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
+    "hk_nll_partials": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "hk_nll_eval": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
+    "hk_model_density": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "hk_yield_partials": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
+    "hk_unweight_flags": (ctypes.c_int, [_P, _I64, ctypes.c_double, _P, _U64, _P, _P, _P, _P]),
+    "hk_compact": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _I32, _P]),
+    "hk_scan_counts": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "hk_sample_pdf": (ctypes.c_int, [_P, _I32, _P, _P, ctypes.c_double, _P, _U64, _I64, _I32, _P, _P, _P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen the library and attach signatures (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise DeviceUnavailable(
+                    f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                    f"g.build()'` (there is no CPU fallback)")
+            lib = ctypes.CDLL(path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(512)
+    load_library().hk_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc != HK_OK:
+        msg = last_error()
+        if rc == HK_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        if rc == HK_EUNSUPPORTED:
+            raise NotImplementedError(f"{what}: {msg}")
+        raise KernelError(f"{what} failed (rc={rc}): {msg}")
+
+
+_torch = None
+
+
+def torch():
+    """Import torch lazily (it is plumbing: allocation, streams, collectives)."""
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def device():
+    """The current CUDA device; raises when there is none (no CPU fallback)."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise DeviceUnavailable("no CUDA device is visible; the hot path has no CPU fallback")
+    load_library()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def lib() -> ctypes.CDLL:
+    device()
+    return _lib
+
+
+def stream_ptr() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def ptr_array(tensors) -> ctypes.Array:
+    arr = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    return arr
+
+
+def empty(n: int, dtype=None):
+    t = torch()
+    return t.empty(int(n), dtype=dtype or t.float64, device=device())
+
+
+def bad_cells(k: int = 1):
+    """k first-bad-row cells initialised to HK_NO_BAD_ROW."""
+    t = torch()
+    return t.full((k,), -1, dtype=t.int64, device=device())
+
+
+def read_bad(cells) -> list[int]:
+    return [int(v) % (1 << 64) for v in cells.cpu().tolist()]
+
+
+def u64(v: int) -> int:
+    return int(v) % (1 << 64)
+
+
+def make_key(key, mode: int = HK_RNG_REFERENCE) -> hk_key_t:
+    return hk_key_t(u64(key.seed), u64(key.stream), u64(key.counter), int(mode), 0)
+
+
+def make_decay(spec, mother=None, m_mother=None) -> hk_decay_t:
+    """hk_decay_t from a DecaySpec; T/csum with numpy like phasespace.py:94-97."""
+    ms = np.asarray(spec.daughter_masses, dtype=np.float64)
+    n = len(ms)
+    if n > HK_MAX_DAUGHTERS:
+        raise NotImplementedError(f"{n} daughters: the library supports up to {HK_MAX_DAUGHTERS}")
+    d = hk_decay_t()
+    d.n = n
+    d.mother_mass = float(spec.mother_mass)
+    d.T = float(spec.mother_mass - float(np.sum(ms)))
+    csum = np.cumsum(ms)
+    for i in range(n):
+        d.masses[i] = float(ms[i])
+        d.csum[i] = float(csum[i])
+    if mother is None:
+        d.moving = 0
+        d.mother[:] = [float(spec.mother_mass), 0.0, 0.0, 0.0]
+        d.m_mother = float(spec.mother_mass)
+    else:
+        d.moving = int(mother.px != 0.0 or mother.py != 0.0 or mother.pz != 0.0)
+        d.mother[:] = [float(mother.e), float(mother.px), float(mother.py), float(mother.pz)]
+        d.m_mother = float(m_mother)
+    return d
+
+
+def num_chunks(n: int) -> int:
+    return (int(n) + HK_CHUNK - 1) // HK_CHUNK
+
+
+def fold(partials, n_parts: int, width: int):
+    """Deterministic device fold of (n_parts, width) partials -> (width,) tensor."""
+    out = empty(width)
+    check(lib().hk_fold_partials(ptr(partials) if n_parts else None, int(n_parts), int(width),
+                                 ptr(out), stream_ptr()), "hk_fold_partials")
+    return out

@@ -1,0 +1,359 @@
+// hk_device.cuh -- device building blocks shared by the sm_100a kernels.
+//
+// Everything here is per-event register arithmetic on the FP64 pipe (the
+// kinematics) and the integer pipe (the counter RNGs); nothing is a dense
+// contraction, so there is no tensor-core work in this library.
+//
+// Parity notes (SURVEY.md 0, 7 "hard parts"):
+//  * translation units that include this header are compiled with
+//    -fmad=false, so every a*b+c below rounds twice exactly like numpy; the
+//    few places that want an FMA spell it out with fma().
+//  * CUDA's sqrt and double division are IEEE correctly rounded, so weights
+//    (products of breakup momenta) are bit-identical to the reference; only
+//    sin/cos differ (<= 1-2 ulp), which moves momentum components by
+//    <~1e-16 * E (the parity tolerance is 1e-12 * E_daughter).
+#pragma once
+
+#include <cstdint>
+
+#include "hepkit_cuda.h"
+
+namespace hk {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;  // rng.py:33
+constexpr uint64_t kMix1 = 0xBF58476D1CE4E5B9ull;    // rng.py:34
+constexpr uint64_t kMix2 = 0x94D049BB133111EBull;    // rng.py:35
+constexpr uint64_t kSalt = 0x6A09E667F3BCC909ull;    // rng.py:36
+constexpr double kInv53 = 1.1102230246251565e-16;    // 2^-53, rng.py:39
+constexpr double kTwoPi = 6.283185307179586;         // fl(2 * pi), phasespace.py:136
+constexpr int kBlock = 256;                          // threads per CTA
+constexpr int kRowsPerThread = HK_CHUNK / kBlock;    // 16 rows per thread per chunk
+
+// ---------------------------------------------------------------- RNG ------
+// SplitMix64 avalanche finalizer (rng.py:98-102).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * kMix1;
+  z = (z ^ (z >> 27)) * kMix2;
+  return z ^ (z >> 31);
+}
+
+// base(seed, stream) (rng.py:109-112); inputs already reduced mod 2^64.
+__host__ __device__ __forceinline__ uint64_t key_base(uint64_t seed, uint64_t stream) {
+  return mix64(seed + kGolden) ^ mix64(stream * kSalt + kGolden);
+}
+
+// top 53 bits -> [0, 1), exact (rng.py:125)
+__device__ __forceinline__ double to_unit(uint64_t bits53) {
+  return __ull2double_rn(bits53) * kInv53;
+}
+
+// Philox4x32-10 (Salmon et al., SC'11); counter = (row lo, row hi, block, tag).
+struct Philox4 {
+  uint32_t v[4];
+};
+
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                 uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  Philox4 out;
+  out.v[0] = c0;
+  out.v[1] = c1;
+  out.v[2] = c2;
+  out.v[3] = c3;
+  return out;
+}
+
+constexpr uint32_t kPhiloxTag = 0x686b7068u;  // "hkph": separates this use of the key
+
+// Per-launch RNG parameters; both modes are derived from the same hk_key_t.
+struct RngParams {
+  uint64_t base;  // SplitMix64 key base (reference mode) / Philox key (philox mode)
+  uint64_t kc;    // key.counter
+  int32_t mode;
+};
+
+inline RngParams make_rng(const hk_key_t& k) {
+  RngParams r;
+  r.base = key_base(k.seed, k.stream);
+  r.kc = k.counter;
+  r.mode = k.mode;
+  return r;
+}
+
+// The D uniforms of one event as 53-bit integers, so the mass uniforms can be
+// ordered on the integer pipe (order of the integers == order of the doubles).
+// Reference mode: counter (row + kc) * D + j (phasespace.py:105-109).
+template <int D, int MODE>
+__device__ __forceinline__ void draw_bits(const RngParams& rp, uint64_t row, uint64_t (&bits)[D]) {
+  if (MODE == HK_RNG_REFERENCE) {
+    const uint64_t x0 = rp.base + (row + rp.kc) * (uint64_t)D * kGolden;
+#pragma unroll
+    for (int j = 0; j < D; ++j) bits[j] = mix64(x0 + (uint64_t)j * kGolden) >> 11;
+  } else {
+    const uint64_t ev = row + rp.kc;
+    const uint32_t k0 = (uint32_t)rp.base, k1 = (uint32_t)(rp.base >> 32);
+#pragma unroll
+    for (int b = 0; b < (D + 1) / 2; ++b) {
+      const Philox4 o = philox4x32_10((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)b, kPhiloxTag,
+                                      k0, k1);
+      bits[2 * b] = (((uint64_t)o.v[0] << 32) | o.v[1]) >> 11;
+      if (2 * b + 1 < D) bits[2 * b + 1] = (((uint64_t)o.v[2] << 32) | o.v[3]) >> 11;
+    }
+  }
+}
+
+// Runtime-D variant for the generic (n > 8) kernels.
+template <int MODE>
+__device__ __forceinline__ uint64_t draw_bit_rt(const RngParams& rp, uint64_t row, int D, int j) {
+  if (MODE == HK_RNG_REFERENCE) {
+    return mix64(rp.base + ((row + rp.kc) * (uint64_t)D + (uint64_t)j) * kGolden) >> 11;
+  } else {
+    const uint64_t ev = row + rp.kc;
+    const Philox4 o = philox4x32_10((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)(j >> 1),
+                                    kPhiloxTag, (uint32_t)rp.base, (uint32_t)(rp.base >> 32));
+    return (j & 1) ? ((((uint64_t)o.v[2] << 32) | o.v[3]) >> 11)
+                   : ((((uint64_t)o.v[0] << 32) | o.v[1]) >> 11);
+  }
+}
+
+// ---------------------------------------------------------- kinematics -----
+// np.maximum(x, 0.0): NaN propagates, -0.0 kept.
+__device__ __forceinline__ double max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
+
+// Two-body breakup momentum (phasespace.py:67-71), reference op order; b2 = m*m
+// of the fixed daughter.
+__device__ __forceinline__ double pstar(double M, double a, double b2) {
+  const double M2 = M * M, a2 = a * a;
+  const double t = (M2 - a2) - b2;
+  const double lam = t * t - (4.0 * a2) * b2;
+  return sqrt(max0(lam)) / (2.0 * M);
+}
+
+// Boost frame of _boost (phasespace.py:74-81): the per-frame factors are shared
+// by every vector boosted into it, which is exact (same operands, same ops).
+struct Frame {
+  double gamma, bx, by, bz, g2;
+};
+
+__device__ __forceinline__ Frame make_frame(double fe, double fx, double fy, double fz,
+                                            double fm) {
+  Frame f;
+  f.gamma = fe / fm;
+  f.bx = fx / fe;
+  f.by = fy / fe;
+  f.bz = fz / fe;
+  f.g2 = f.gamma * f.gamma / (f.gamma + 1.0);
+  return f;
+}
+
+__device__ __forceinline__ void boost(const Frame& f, double& e, double& px, double& py,
+                                      double& pz) {
+  const double bp = f.bx * px + f.by * py + f.bz * pz;
+  const double k = f.g2 * bp + f.gamma * e;
+  e = f.gamma * (e + bp);
+  px = px + k * f.bx;
+  py = py + k * f.by;
+  pz = pz + k * f.bz;
+}
+
+// compare-exchange on the integer pipe
+__device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
+  const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+  a = lo;
+  b = hi;
+}
+
+// One event of the rest-frame generator (phasespace.py:103-149) for a
+// compile-time daughter count N.  p[4j..4j+3] = (e, px, py, pz) of daughter
+// j+1; returns the weight (product of breakup momenta, phasespace.py:120-125).
+template <int N, int MODE>
+__device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParams& rp,
+                                             uint64_t row, double (&p)[4 * N]) {
+  constexpr int D = 3 * N - 4;  // phasespace.py:84-86
+  uint64_t bits[D];
+  draw_bits<D, MODE>(rp, row, bits);
+  // sorted mass uniforms: odd-even transposition network, integer compares
+#pragma unroll
+  for (int pass = 0; pass < N - 2; ++pass) {
+#pragma unroll
+    for (int j = pass & 1; j + 1 < N - 2; j += 2) cswap(bits[j], bits[j + 1]);
+  }
+  double inv[N];
+  inv[0] = d.csum[0];  // 0 * T + csum[0] is exact
+#pragma unroll
+  for (int k = 1; k < N - 1; ++k) inv[k] = to_unit(bits[k - 1]) * d.T + d.csum[k];
+  inv[N - 1] = d.T + d.csum[N - 1];  // 1.0 * T + csum[n-1] (phasespace.py:118)
+
+  double ps[N];
+  double w = 1.0;
+#pragma unroll
+  for (int k = 1; k < N; ++k) {
+    ps[k] = pstar(inv[k], inv[k - 1], d.masses[k] * d.masses[k]);
+    w = w * ps[k];
+  }
+
+  p[0] = d.masses[0];
+  p[1] = 0.0;
+  p[2] = 0.0;
+  p[3] = 0.0;
+#pragma unroll
+  for (int k = 1; k < N; ++k) {
+    const double q = ps[k];
+    const double cz = 2.0 * to_unit(bits[N - 2 + 2 * (k - 1)]) - 1.0;
+    const double phi = kTwoPi * to_unit(bits[N - 2 + 2 * (k - 1) + 1]);
+    const double sz = sqrt(max0(1.0 - cz * cz));
+    double sn, cs;
+    sincos(phi, &sn, &cs);
+    const double nx = sz * cs, ny = sz * sn, nz = cz;
+    const double clm = inv[k - 1];
+    const double cle = sqrt(q * q + clm * clm);
+    const double clx = q * nx, cly = q * ny, clz = q * nz;
+    const Frame f = make_frame(cle, clx, cly, clz, clm);
+#pragma unroll
+    for (int j = 0; j < k; ++j) boost(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+    p[4 * k + 0] = sqrt(q * q + d.masses[k] * d.masses[k]);
+    p[4 * k + 1] = -clx;
+    p[4 * k + 2] = -cly;
+    p[4 * k + 3] = -clz;
+  }
+  return w;
+}
+
+// Runtime-n variant (n <= HK_MAX_DAUGHTERS); arrays live in local memory.
+template <int MODE>
+__device__ double rest_event_rt(const hk_decay_t& d, const RngParams& rp, uint64_t row,
+                                double* p) {
+  const int n = d.n, D = 3 * n - 4;
+  double rno[HK_MAX_DAUGHTERS], inv[HK_MAX_DAUGHTERS], ps[HK_MAX_DAUGHTERS];
+  uint64_t sorted[HK_MAX_DAUGHTERS];
+  for (int j = 0; j < n - 2; ++j) {  // insertion sort of the mass uniforms
+    const uint64_t b = draw_bit_rt<MODE>(rp, row, D, j);
+    int i = j;
+    while (i > 0 && sorted[i - 1] > b) {
+      sorted[i] = sorted[i - 1];
+      --i;
+    }
+    sorted[i] = b;
+  }
+  for (int k = 1; k < n - 1; ++k) rno[k] = to_unit(sorted[k - 1]);
+  inv[0] = d.csum[0];
+  for (int k = 1; k < n - 1; ++k) inv[k] = rno[k] * d.T + d.csum[k];
+  inv[n - 1] = d.T + d.csum[n - 1];
+  double w = 1.0;
+  for (int k = 1; k < n; ++k) {
+    ps[k] = pstar(inv[k], inv[k - 1], d.masses[k] * d.masses[k]);
+    w = w * ps[k];
+  }
+  p[0] = d.masses[0];
+  p[1] = p[2] = p[3] = 0.0;
+  for (int k = 1; k < n; ++k) {
+    const double q = ps[k];
+    const double cz = 2.0 * to_unit(draw_bit_rt<MODE>(rp, row, D, n - 2 + 2 * (k - 1))) - 1.0;
+    const double phi = kTwoPi * to_unit(draw_bit_rt<MODE>(rp, row, D, n - 1 + 2 * (k - 1)));
+    const double sz = sqrt(max0(1.0 - cz * cz));
+    double sn, cs;
+    sincos(phi, &sn, &cs);
+    const double clm = inv[k - 1];
+    const double cle = sqrt(q * q + clm * clm);
+    const double clx = q * (sz * cs), cly = q * (sz * sn), clz = q * cz;
+    const Frame f = make_frame(cle, clx, cly, clz, clm);
+    for (int j = 0; j < k; ++j) boost(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+    p[4 * k + 0] = sqrt(q * q + d.masses[k] * d.masses[k]);
+    p[4 * k + 1] = -clx;
+    p[4 * k + 2] = -cly;
+    p[4 * k + 3] = -clz;
+  }
+  return w;
+}
+
+// -------------------------------------------------------- reductions -------
+// Deterministic CTA reduction of W doubles: fixed shuffle tree inside each
+// warp, then warps summed in index order by thread w.  Writes out[0..W).
+template <int W>
+__device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
+  __shared__ double sm[kBlock / 32][W];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] += __shfl_down_sync(0xffffffffu, v[w], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) sm[warp][w] = v[w];
+  }
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double s = sm[0][threadIdx.x];
+#pragma unroll
+    for (int i = 1; i < kBlock / 32; ++i) s += sm[i][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void record_bad(unsigned long long* first_bad, uint64_t row) {
+  if (first_bad) atomicMin(first_bad, (unsigned long long)row);
+}
+
+// -------------------------------------------------- functor programs -------
+// Interpreter for hk_program_t (host-lowered FunctorExpr + arg_builder DAG).
+// Every thread runs the same op stream, so the switch is warp-uniform.
+// `load(c)` supplies column c of the current event.  Division by zero sets
+// *div0 (functors.py:200-207 raises before evaluating).
+template <class Load>
+__device__ __forceinline__ double run_program(const hk_program_t& P, Load load, bool* div0) {
+  double r[HK_MAX_SLOTS];
+  for (int i = 0; i < P.n_ops; ++i) {
+    const int op = P.op[i];
+    double v;
+    switch (op) {
+      case HK_OP_COL: v = load(P.a[i]); break;
+      case HK_OP_CONST: v = P.cst[i]; break;
+      case HK_OP_ADD: v = r[P.a[i]] + r[P.b[i]]; break;
+      case HK_OP_SUB: v = r[P.a[i]] - r[P.b[i]]; break;
+      case HK_OP_MUL: v = r[P.a[i]] * r[P.b[i]]; break;
+      case HK_OP_DIV: {
+        const double den = r[P.b[i]];
+        if (den == 0.0) *div0 = true;
+        v = r[P.a[i]] / den;
+        break;
+      }
+      case HK_OP_NEG: v = -r[P.a[i]]; break;
+      case HK_OP_SQRT: v = sqrt(r[P.a[i]]); break;
+      case HK_OP_EXP: v = exp(r[P.a[i]]); break;
+      case HK_OP_LOG: v = log(r[P.a[i]]); break;
+      case HK_OP_GAUSS: {
+        const double s = P.cst2[i];
+        const double z = (r[P.a[i]] - P.cst[i]) / s;
+        v = exp(-0.5 * z * z) / (s * 2.5066282746310002);  // functors.py:26, :142-143
+        break;
+      }
+      case HK_OP_EXPO: v = exp(-r[P.a[i]] / P.cst[i]); break;
+      case HK_OP_BW: {
+        const double m0 = P.cst[i], g0 = P.cst2[i];
+        const double t = r[P.a[i]] - m0 * m0;
+        v = 1.0 / (t * t + (m0 * m0) * (g0 * g0));
+        break;
+      }
+      case HK_OP_ADD0: v = r[P.a[i]] + 0.0; break;
+      case HK_OP_SQUARE: v = r[P.a[i]] * r[P.a[i]]; break;
+      default: v = __longlong_as_double(0x7ff8000000000000ll); break;
+    }
+    r[P.dst[i]] = v;
+  }
+  return r[P.result];
+}
+
+}  // namespace hk

@@ -1,0 +1,300 @@
+// hk_fcn.cu -- the unbinned extended NLL (FCN) event sum for sm_100a.
+//
+// nll = sum_k N_k - sum_e ln(sum_k N_k shape_k(x_e) / norm_k)   (fitting.py:175-210)
+//
+// The host computes the norms (fitting.py:80-89, 103-123) and the
+// expected total; this kernel does the data pass: fused p.d.f. evaluation ->
+// density -> positivity check -> log -> fixed-order CTA sum per 4096-row
+// chunk.  The per-component constants are folded on the host
+// (A_k = N_k / (sigma_k sqrt(2 pi) norm_k), 1/sigma_k, -1/tau_k), which moves a
+// density by a few ulp -- far inside the 1e-10 FCN tolerance -- and leaves
+// two exp, one log and ~12 DFMA-class ops per event: FP64-pipe bound, with
+// the 8 B/event column usually L2-resident (1e7 events = 80 MB < 126 MB L2).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "hepkit_cuda.h"
+#include "hk_device.cuh"
+#include "hk_host.h"
+
+namespace hk {
+
+struct Coeffs {
+  int32_t n_comp;
+  int32_t kind[HK_MAX_COMPONENTS];
+  double amp[HK_MAX_COMPONENTS];    // gauss: N/(s*sqrt(2pi)*norm); expo: N/norm
+  double shift[HK_MAX_COMPONENTS];  // gauss: mean
+  double scale[HK_MAX_COMPONENTS];  // gauss: 1/sigma; expo: -1/tau
+};
+
+__device__ __forceinline__ double density(const Coeffs& c, double x) {
+  double d = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < c.n_comp; ++k) {
+    double t;
+    if (c.kind[k] == HK_SHAPE_GAUSS) {
+      const double z = (x - c.shift[k]) * c.scale[k];
+      t = c.amp[k] * exp(-0.5 * z * z);
+    } else {
+      t = c.amp[k] * exp(x * c.scale[k]);
+    }
+    d = k == 0 ? t : d + t;
+  }
+  return d;
+}
+
+// Two-component Gaussian + exponential specialisation (the benchmark model,
+// cli.py:316-320 / toymodel.py): no component loop, no kind branches.
+__device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
+  const double z = (x - c.shift[0]) * c.scale[0];
+  return c.amp[0] * exp(-0.5 * z * z) + c.amp[1] * exp(x * c.scale[1]);
+}
+
+template <bool GE>
+__global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, int64_t n,
+                                                const __grid_constant__ Coeffs c,
+                                                double* __restrict__ part,
+                                                unsigned long long* first_bad) {
+  const int64_t chunks = (n + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    double acc[1] = {0.0};
+    const int64_t r0 = ch * HK_CHUNK + threadIdx.x;
+    if (ch * HK_CHUNK + HK_CHUNK <= n) {
+      // full chunk: issue all 16 loads first (MLP), then the math
+      double xv[kRowsPerThread];
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const double d = GE ? density_ge(c, xv[i]) : density(c, xv[i]);
+        if (!(d > 0.0) || !isfinite(d)) record_bad(first_bad, (uint64_t)(r0 + i * kBlock));
+        acc[0] += log(d);
+      }
+    } else {
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const int64_t r = r0 + i * kBlock;
+        if (r < n) {
+          const double xr = __ldg(x + r);
+          const double d = GE ? density_ge(c, xr) : density(c, xr);
+          if (!(d > 0.0) || !isfinite(d)) record_bad(first_bad, (uint64_t)r);
+          acc[0] += log(d);
+        }
+      }
+    }
+    block_sum_store<1>(acc, part + ch);
+  }
+}
+
+// Reference op order (fitting.py:160-166, functors.py:142-143, :161) with no
+// contraction -- used only for the value quoted in the error message.
+__global__ void k_density_exact(const double* x, int64_t n, const __grid_constant__ hk_model_t m,
+                                double* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xv = x[i];
+  double d = 0.0;
+  for (int k = 0; k < m.n_comp; ++k) {
+    double shape;
+    if (m.kind[k] == HK_SHAPE_GAUSS) {
+      const double s = m.p1[k];
+      const double z = (xv - m.p0[k]) / s;
+      shape = exp(__dmul_rn(-0.5 * z, z)) / __dmul_rn(s, 2.5066282746310002);
+    } else {
+      shape = exp(-xv / m.p0[k]);
+    }
+    const double t = __dmul_rn(m.yield[k], shape / m.norm[k]);
+    d = k == 0 ? t : __dadd_rn(d, t);
+  }
+  out[i] = d;
+}
+
+int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStream_t st);
+
+// pdf_k(x) = shape_k(x)/norm_k without the yield (fitting.py:91-92)
+struct PdfCoeffs {
+  int32_t kind[4];
+  double amp[4], shift[4], scale[4], yield[4];
+};
+
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_yield(const double* __restrict__ x, int64_t n,
+                                                  const __grid_constant__ PdfCoeffs c,
+                                                  double* __restrict__ part,
+                                                  unsigned long long* first_bad) {
+  constexpr int W = K + K * K;
+  const int64_t chunks = (n + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    double acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = ch * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r >= n) continue;
+      const double xv = __ldg(x + r);
+      double p[K], d = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (c.kind[k] == HK_SHAPE_GAUSS) {
+          const double z = (xv - c.shift[k]) * c.scale[k];
+          p[k] = c.amp[k] * exp(-0.5 * z * z);
+        } else {
+          p[k] = c.amp[k] * exp(xv * c.scale[k]);
+        }
+        d += p[k] * c.yield[k];
+      }
+      if (!(d > 0.0)) record_bad(first_bad, (uint64_t)r);
+      const double inv = 1.0 / d;
+#pragma unroll
+      for (int k = 0; k < K; ++k) p[k] *= inv;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc[k] += p[k];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[K + k * K + j] += p[k] * p[j];
+      }
+    }
+    block_sum_store<W>(acc, part + (int64_t)W * ch);
+  }
+}
+
+int make_coeffs(const hk_model_t* m, Coeffs* c) {
+  HK_REQUIRE(m != nullptr, "NULL model");
+  HK_REQUIRE(m->n_comp >= 1 && m->n_comp <= HK_MAX_COMPONENTS, "component count %d outside 1..%d",
+             m->n_comp, HK_MAX_COMPONENTS);
+  std::memset(c, 0, sizeof(*c));
+  c->n_comp = m->n_comp;
+  const double sqrt2pi = 2.5066282746310002;  // functors.py:26
+  for (int k = 0; k < m->n_comp; ++k) {
+    c->kind[k] = m->kind[k];
+    if (m->kind[k] == HK_SHAPE_GAUSS) {
+      HK_REQUIRE(m->p1[k] > 0, "component %d: sigma must be positive, got %g", k, m->p1[k]);
+      c->amp[k] = m->yield[k] / (m->p1[k] * sqrt2pi * m->norm[k]);
+      c->shift[k] = m->p0[k];
+      c->scale[k] = 1.0 / m->p1[k];
+    } else if (m->kind[k] == HK_SHAPE_EXPO) {
+      HK_REQUIRE(m->p0[k] != 0, "component %d: tau must be non-zero", k);
+      c->amp[k] = m->yield[k] / m->norm[k];
+      c->scale[k] = -1.0 / m->p0[k];
+    } else {
+      set_error("component %d: unknown shape kind %d", k, m->kind[k]);
+      return HK_EUNSUPPORTED;
+    }
+  }
+  return HK_OK;
+}
+
+int launch_nll(const double* d_x, int64_t n, const Coeffs& c, double* part,
+               unsigned long long* bad, cudaStream_t st) {
+  const unsigned grid = chunk_grid(num_chunks(n));
+  const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
+  if (ge)
+    k_nll<true><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad);
+  else
+    k_nll<false><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad);
+  return check_launch("k_nll");
+}
+
+// small pinned readback cell per host thread for hk_nll_eval
+struct Readback {
+  double* h = nullptr;
+  ~Readback() {
+    if (h) cudaFreeHost(h);
+  }
+};
+
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
+                    uint64_t* d_first_bad, void* stream) {
+  Coeffs c;
+  if (int rc = make_coeffs(model, &c)) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_x && d_partials, "NULL pointer");
+  return launch_nll(d_x, n, c, d_partials, reinterpret_cast<unsigned long long*>(d_first_bad),
+                    as_stream(stream));
+}
+
+int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
+                double* h_logsum, uint64_t* h_first_bad, void* stream) {
+  Coeffs c;
+  if (int rc = make_coeffs(model, &c)) return rc;
+  HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
+  HK_REQUIRE(d_x && d_work && h_logsum && h_first_bad, "NULL pointer");
+  cudaStream_t st = as_stream(stream);
+  const int64_t chunks = num_chunks(n);
+  // d_work layout: [0] fold output, [1] first-bad cell (u64), [2..] partials
+  double* out = d_work;
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(d_work + 1);
+  double* part = d_work + 2;
+  HK_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  if (int rc = launch_nll(d_x, n, c, part, bad, st)) return rc;
+  if (int rc = launch_fold(part, chunks, 1, out, st)) return rc;
+  thread_local Readback rb;
+  if (!rb.h) HK_CUDA(cudaMallocHost(&rb.h, 2 * sizeof(double)));
+  HK_CUDA(cudaMemcpyAsync(rb.h, d_work, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  HK_CUDA(cudaStreamSynchronize(st));
+  *h_logsum = rb.h[0];
+  std::memcpy(h_first_bad, &rb.h[1], sizeof(uint64_t));
+  return HK_OK;
+}
+
+int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
+                      uint64_t* d_first_bad, void* stream) {
+  HK_REQUIRE(model && model->n_comp >= 1 && model->n_comp <= 4,
+             "yield stationarity supports 1..4 components");
+  PdfCoeffs c;
+  std::memset(&c, 0, sizeof(c));
+  const double sqrt2pi = 2.5066282746310002;
+  for (int k = 0; k < model->n_comp; ++k) {
+    c.kind[k] = model->kind[k];
+    c.yield[k] = model->yield[k];
+    if (model->kind[k] == HK_SHAPE_GAUSS) {
+      HK_REQUIRE(model->p1[k] > 0, "component %d: sigma must be positive", k);
+      c.amp[k] = 1.0 / (model->p1[k] * sqrt2pi * model->norm[k]);
+      c.shift[k] = model->p0[k];
+      c.scale[k] = 1.0 / model->p1[k];
+    } else if (model->kind[k] == HK_SHAPE_EXPO) {
+      HK_REQUIRE(model->p0[k] != 0, "component %d: tau must be non-zero", k);
+      c.amp[k] = 1.0 / model->norm[k];
+      c.scale[k] = -1.0 / model->p0[k];
+    } else {
+      set_error("component %d: unknown shape kind %d", k, model->kind[k]);
+      return HK_EUNSUPPORTED;
+    }
+  }
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_x && d_partials, "NULL pointer");
+  const unsigned grid = chunk_grid(num_chunks(n));
+  cudaStream_t st = as_stream(stream);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  switch (model->n_comp) {
+    case 1: k_yield<1><<<grid, kBlock, 0, st>>>(d_x, n, c, d_partials, bad); break;
+    case 2: k_yield<2><<<grid, kBlock, 0, st>>>(d_x, n, c, d_partials, bad); break;
+    case 3: k_yield<3><<<grid, kBlock, 0, st>>>(d_x, n, c, d_partials, bad); break;
+    default: k_yield<4><<<grid, kBlock, 0, st>>>(d_x, n, c, d_partials, bad); break;
+  }
+  return check_launch("k_yield");
+}
+
+int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,
+                     void* stream) {
+  Coeffs c;
+  if (int rc = make_coeffs(model, &c)) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_x && d_out, "NULL pointer");
+  k_density_exact<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_x, n, *model,
+                                                                               d_out);
+  return check_launch("k_density_exact");
+}
+
+}  // extern "C"

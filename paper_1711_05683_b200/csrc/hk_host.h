@@ -1,0 +1,49 @@
+// hk_host.h -- host-side helpers shared by the C-ABI translation units:
+// per-thread error text, CUDA status checks, launch-shape helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+
+#include "hepkit_cuda.h"
+
+namespace hk {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* where);
+
+inline int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HK_OK : cuda_fail(e, where);
+}
+
+inline int64_t num_chunks(int64_t n) { return n <= 0 ? 0 : (n + HK_CHUNK - 1) / HK_CHUNK; }
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Grid for chunk-per-CTA kernels.  One CTA per 4096-row chunk; the hardware
+// block scheduler load-balances the waves.  gridDim.x is capped and kernels
+// grid-stride over chunks beyond the cap.
+inline unsigned chunk_grid(int64_t chunks) {
+  const int64_t cap = int64_t(1) << 30;
+  return (unsigned)(chunks < 1 ? 1 : (chunks > cap ? cap : chunks));
+}
+
+}  // namespace hk
+
+#define HK_REQUIRE(cond, ...)       \
+  do {                              \
+    if (!(cond)) {                  \
+      ::hk::set_error(__VA_ARGS__); \
+      return HK_EINVAL;             \
+    }                               \
+  } while (0)
+
+#define HK_CUDA(call)                                                  \
+  do {                                                                 \
+    cudaError_t hk_e_ = (call);                                        \
+    if (hk_e_ != cudaSuccess) return ::hk::cuda_fail(hk_e_, #call);    \
+  } while (0)

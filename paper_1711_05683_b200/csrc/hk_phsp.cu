@@ -1,0 +1,844 @@
+// hk_phsp.cu -- phase-space generation, decay chains, phase-space averages
+// and unweighting for sm_100a.  Compiled with -fmad=false (see hk_device.cuh).
+//
+// Layout in HBM: one contiguous fp64 column per schema field (phsp_schema,
+// phasespace.py:60-64), owned by the caller (torch tensors on the Python side).
+// A CTA owns one 4096-row chunk (parallel.py:18); its 256 threads walk the
+// chunk in 16 row-strided steps so every column store is a fully coalesced
+// 256 B warp transaction, and the chunk's moment partial is a fixed-order
+// CTA reduction -- the GPU analogue of the reference's chunk partials.
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "hepkit_cuda.h"
+#include "hk_device.cuh"
+#include "hk_host.h"
+
+namespace hk {
+
+constexpr int kMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
+constexpr int kFastMaxN = 8;  // templated register-resident kernels for n <= 8
+
+struct GenArgs {
+  hk_decay_t d;
+  RngParams rp;
+  uint64_t ev_begin;
+  int64_t count;
+  double* cols[kMaxCols];  // all NULL = no store
+  double* wpart;           // 2 doubles per chunk or NULL
+  int store;
+};
+
+// ------------------------------------------------------------ generation ---
+template <int N, int MODE>
+__global__ void __launch_bounds__(kBlock) k_generate(const __grid_constant__ GenArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  Frame mf{};
+  if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
+                                  a.d.m_mother);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[2] = {0.0, 0.0};
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.count) {
+        double p[4 * N];
+        const double w = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r, p);
+        if (a.d.moving) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        }
+        if (a.store) {
+          __stcs(a.cols[0] + r, w);
+#pragma unroll
+          for (int j = 0; j < 4 * N; ++j) __stcs(a.cols[1 + j] + r, p[j]);
+        }
+        acc[0] += w;
+        acc[1] += w * w;
+      }
+    }
+    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_generate_rt(const __grid_constant__ GenArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  const int n = a.d.n;
+  Frame mf{};
+  if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
+                                  a.d.m_mother);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[2] = {0.0, 0.0};
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.count) {
+        double p[4 * HK_MAX_DAUGHTERS];
+        const double w = rest_event_rt<MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r, p);
+        if (a.d.moving)
+          for (int j = 0; j < n; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        if (a.store) {
+          __stcs(a.cols[0] + r, w);
+          for (int j = 0; j < 4 * n; ++j) __stcs(a.cols[1 + j] + r, p[j]);
+        }
+        acc[0] += w;
+        acc[1] += w * w;
+      }
+    }
+    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+  }
+}
+
+// ---------------------------------------------------- fused integration ----
+struct IntArgs {
+  hk_decay_t d;
+  RngParams rp;
+  uint64_t ev_begin;
+  int64_t count;
+  hk_program_t f;
+  double* part;  // 5 doubles per chunk
+  unsigned long long* div0_bad;
+  unsigned long long* nonfinite_bad;
+};
+
+// phsp_generate -> phsp_average (phasespace.py:162-188 then :310-349) with the
+// event kept in registers: 0 bytes of HBM per event.
+template <int N, int MODE>
+__global__ void __launch_bounds__(kBlock) k_integrate(const __grid_constant__ IntArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  Frame mf{};
+  if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
+                                  a.d.m_mother);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.count) {
+        const uint64_t row = a.ev_begin + (uint64_t)r;
+        double v[4 * N + 1];
+        double p[4 * N];
+        const double w = rest_event<N, MODE>(a.d, a.rp, row, p);
+        if (a.d.moving) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        }
+        v[0] = w;
+#pragma unroll
+        for (int j = 0; j < 4 * N; ++j) v[1 + j] = p[j];
+        bool div0 = false;
+        const double f = run_program(a.f, [&](int col) { return v[col]; }, &div0);
+        if (div0) record_bad(a.div0_bad, row);
+        if (!isfinite(f)) record_bad(a.nonfinite_bad, row);
+        const double ww = w * w;
+        acc[0] += w;
+        acc[1] += w * f;
+        acc[2] += ww;
+        acc[3] += ww * f;
+        acc[4] += ww * f * f;
+      }
+    }
+    block_sum_store<5>(acc, a.part + 5 * c);
+  }
+}
+
+// ------------------------------------------- moments over stored columns ---
+struct MomArgs {
+  const double* cols[kMaxCols];
+  int32_t n_cols;
+  int64_t count;
+  hk_program_t f;
+  double* part;
+  unsigned long long* div0_bad;
+  unsigned long long* nonfinite_bad;
+};
+
+// phsp_average over a stored block (phasespace.py:310-329): f from the
+// program over the event's columns, then the five chunk moments.
+__global__ void __launch_bounds__(kBlock) k_moments(const __grid_constant__ MomArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.count) {
+        bool div0 = false;
+        const double f = run_program(a.f, [&](int col) { return __ldg(a.cols[col] + r); }, &div0);
+        if (div0) record_bad(a.div0_bad, (uint64_t)r);
+        if (!isfinite(f)) record_bad(a.nonfinite_bad, (uint64_t)r);
+        const double w = __ldg(a.cols[0] + r);
+        const double ww = w * w;
+        acc[0] += w;
+        acc[1] += w * f;
+        acc[2] += ww;
+        acc[3] += ww * f;
+        acc[4] += ww * f * f;
+      }
+    }
+    block_sum_store<5>(acc, a.part + 5 * c);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_map(const __grid_constant__ MomArgs a, double* out) {
+  const int64_t r = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (r >= a.count) return;
+  bool div0 = false;
+  out[r] = run_program(a.f, [&](int col) { return __ldg(a.cols[col] + r); }, &div0);
+  if (div0) record_bad(a.div0_bad, (uint64_t)r);
+}
+
+// --------------------------------------------------------- decay chains ----
+struct ChainArgs {
+  hk_decay_t sub;
+  RngParams rp;
+  uint64_t ev_begin;
+  int64_t count;
+  const double* w_in;
+  const double* p4_in[4];
+  double* w_out;
+  double* sub_cols[4 * HK_MAX_DAUGHTERS];
+  unsigned long long* first_bad;
+};
+
+// daughter mass from its four columns (phasespace.py:259-260) + check (:261-262)
+__device__ __forceinline__ double frame_mass(double fe, double fx, double fy, double fz) {
+  return sqrt(max0(fe * fe - fx * fx - fy * fy - fz * fz));
+}
+
+__device__ __forceinline__ bool mass_mismatch(double fm, double M) {
+  const double tol = 1e-9 * (M > 1e-6 ? M : 1e-6);  // MASS_TOLERANCE * max(M, 1e-6)
+  return fabs(fm - M) > tol;                         // NaN compares false, as in numpy
+}
+
+template <int NS, int MODE>
+__global__ void __launch_bounds__(kBlock) k_chain(const __grid_constant__ ChainArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r >= a.count) continue;
+      const uint64_t row = a.ev_begin + (uint64_t)r;
+      const double fe = __ldg(a.p4_in[0] + r), fx = __ldg(a.p4_in[1] + r);
+      const double fy = __ldg(a.p4_in[2] + r), fz = __ldg(a.p4_in[3] + r);
+      const double fm = frame_mass(fe, fx, fy, fz);
+      if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
+      double q[4 * NS];
+      const double ws = rest_event<NS, MODE>(a.sub, a.rp, row, q);
+      const Frame f = make_frame(fe, fx, fy, fz, fm);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) boost(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+      __stcs(a.w_out + r, __ldg(a.w_in + r) * ws);
+#pragma unroll
+      for (int j = 0; j < 4 * NS; ++j) __stcs(a.sub_cols[j] + r, q[j]);
+    }
+  }
+}
+
+struct GenChainArgs {
+  hk_decay_t d;
+  hk_decay_t sub;
+  RngParams rp;
+  RngParams rp_sub;
+  int32_t k;  // 0-based daughter that decays
+  uint64_t ev_begin;
+  int64_t count;
+  double* cols[kMaxCols];  // spliced schema order
+  double* wpart;
+  unsigned long long* first_bad;
+};
+
+// Fused phsp_generate + phsp_decay_chain (config C3): only the 4(n-1+n_sub)+1
+// final-state columns ever touch HBM.
+template <int N, int NS, int MODE>
+__global__ void __launch_bounds__(kBlock) k_generate_chain(const __grid_constant__ GenChainArgs a) {
+  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  Frame mf{};
+  if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
+                                  a.d.m_mother);
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[2] = {0.0, 0.0};
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.count) {
+        const uint64_t row = a.ev_begin + (uint64_t)r;
+        double p[4 * N];
+        const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
+        if (a.d.moving) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        }
+        double fe = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          if (j == a.k) {
+            fe = p[4 * j];
+            fx = p[4 * j + 1];
+            fy = p[4 * j + 2];
+            fz = p[4 * j + 3];
+          }
+        }
+        const double fm = frame_mass(fe, fx, fy, fz);
+        if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
+        double q[4 * NS];
+        const double ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
+        const Frame f = make_frame(fe, fx, fy, fz, fm);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) boost(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+        const double w = wp * ws;
+        __stcs(a.cols[0] + r, w);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          if (j == a.k) continue;
+          const int slot = 1 + 4 * (j < a.k ? j : j + NS - 1);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) __stcs(a.cols[slot + cc] + r, p[4 * j + cc]);
+        }
+        const int sbase = 1 + 4 * a.k;
+#pragma unroll
+        for (int j = 0; j < 4 * NS; ++j) __stcs(a.cols[sbase + j] + r, q[j]);
+        acc[0] += w;
+        acc[1] += w * w;
+      }
+    }
+    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+  }
+}
+
+// ------------------------------------------------------------ unweighting --
+struct UnwArgs {
+  const double* w;
+  int64_t n;
+  double w_max;
+  RngParams rp;
+  uint64_t ev_begin;
+  uint8_t* flags;
+  long long* counts;
+  unsigned long long* first_bad;
+};
+
+__global__ void __launch_bounds__(kBlock) k_unweight_flags(const __grid_constant__ UnwArgs a) {
+  const int64_t chunks = (a.n + HK_CHUNK - 1) / HK_CHUNK;
+  __shared__ int sm[kBlock / 32];
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    int cnt = 0;
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r < a.n) {
+        const uint64_t row = a.ev_begin + (uint64_t)r;
+        const double w = __ldg(a.w + r);
+        if (w > a.w_max) record_bad(a.first_bad, row);
+        // uniform at counter row + key.counter (phasespace.py:226)
+        const double u = to_unit(mix64(a.rp.base + (row + a.rp.kc) * kGolden) >> 11);
+        const bool acc = u * a.w_max < w;
+        a.flags[r] = acc ? 1 : 0;
+        cnt += acc ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long s = 0;
+      for (int k = 0; k < kBlock / 32; ++k) s += sm[k];
+      a.counts[c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// exclusive scan of per-chunk counts by one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan_counts(const long long* in, int64_t n,
+                                                      long long* out, long long* total) {
+  __shared__ long long sm[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t lo = t * per, hi = lo + per < n ? lo + per : n;
+  long long s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += in[i];
+  sm[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
+    long long v = t >= off ? sm[t - off] : 0;
+    __syncthreads();
+    sm[t] += v;
+    __syncthreads();
+  }
+  long long run = t == 0 ? 0 : sm[t - 1];
+  for (int64_t i = lo; i < hi; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  if (t == 1023) *total = sm[1023];
+}
+
+struct CompactArgs {
+  const double* in[kMaxCols];
+  double* out[kMaxCols];
+  int32_t n_cols;
+  int32_t weight_col;
+  int64_t n;
+  const uint8_t* flags;
+  const long long* offsets;
+};
+
+// order-preserving compaction: thread t owns 16 consecutive rows of the chunk
+__global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ CompactArgs a) {
+  const int64_t chunks = (a.n + HK_CHUNK - 1) / HK_CHUNK;
+  __shared__ int sm[kBlock];
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int64_t r0 = c * HK_CHUNK + (int64_t)threadIdx.x * kRowsPerThread;
+    unsigned mask = 0;
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = r0 + i;
+      if (r < a.n && a.flags[r]) mask |= 1u << i;
+    }
+    sm[threadIdx.x] = __popc(mask);
+    __syncthreads();
+    for (int off = 1; off < kBlock; off <<= 1) {
+      int v = threadIdx.x >= (unsigned)off ? sm[threadIdx.x - off] : 0;
+      __syncthreads();
+      sm[threadIdx.x] += v;
+      __syncthreads();
+    }
+    int64_t dst = a.offsets[c] + (threadIdx.x == 0 ? 0 : sm[threadIdx.x - 1]);
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      if (!(mask & (1u << i))) continue;
+      const int64_t r = r0 + i;
+      for (int col = 0; col < a.n_cols; ++col)
+        a.out[col][dst] = col == a.weight_col ? 1.0 : a.in[col][r];
+      ++dst;
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------------- RNG --
+__global__ void k_rng(RngParams rp, const uint64_t* ctr, int64_t n, uint64_t* raw, double* uni) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t c = ctr[i] + rp.kc;
+  uint64_t bits;
+  if (rp.mode == HK_RNG_REFERENCE) {
+    const uint64_t r = mix64(rp.base + c * kGolden);
+    if (raw) raw[i] = r;
+    bits = r >> 11;
+  } else {
+    const Philox4 o = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), 0u, kPhiloxTag,
+                                    (uint32_t)rp.base, (uint32_t)(rp.base >> 32));
+    const uint64_t r = ((uint64_t)o.v[0] << 32) | o.v[1];
+    if (raw) raw[i] = r;
+    bits = r >> 11;
+  }
+  if (uni) uni[i] = to_unit(bits);
+}
+
+// ----------------------------------------------------------------- folds ---
+// Deterministic fold: thread t sums parts t, t+1024, ... in order, then a
+// fixed shuffle/smem tree.  Same n_parts -> same bits, whatever produced them.
+__global__ void __launch_bounds__(1024) k_fold(const double* parts, int64_t n, int width,
+                                               double* out) {
+  __shared__ double sm[32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int w = 0; w < width; ++w) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += 1024) s += parts[i * width + w];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if (lane == 0) sm[warp][w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < width) {
+    double s = sm[0][threadIdx.x];
+    for (int k = 1; k < 32; ++k) s += sm[k][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStream_t st) {
+  k_fold<<<1, 1024, 0, st>>>(parts, n, width, out);
+  return check_launch("k_fold");
+}
+
+// ------------------------------------------------------ launch dispatch ----
+template <int MODE>
+int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
+  switch (a.d.n) {
+#define HK_GEN_CASE(NN) \
+  case NN: k_generate<NN, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    HK_GEN_CASE(2)
+    HK_GEN_CASE(3)
+    HK_GEN_CASE(4)
+    HK_GEN_CASE(5)
+    HK_GEN_CASE(6)
+    HK_GEN_CASE(7)
+    HK_GEN_CASE(8)
+#undef HK_GEN_CASE
+    default: k_generate_rt<MODE><<<grid, kBlock, 0, st>>>(a); break;
+  }
+  return check_launch("k_generate");
+}
+
+template <int MODE>
+int dispatch_integrate(const IntArgs& a, unsigned grid, cudaStream_t st) {
+  switch (a.d.n) {
+#define HK_INT_CASE(NN) \
+  case NN: k_integrate<NN, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    HK_INT_CASE(2)
+    HK_INT_CASE(3)
+    HK_INT_CASE(4)
+    HK_INT_CASE(5)
+    HK_INT_CASE(6)
+    HK_INT_CASE(7)
+    HK_INT_CASE(8)
+#undef HK_INT_CASE
+    default:
+      set_error("fused integration supports 2..%d daughters, got %d", kFastMaxN, a.d.n);
+      return HK_EUNSUPPORTED;
+  }
+  return check_launch("k_integrate");
+}
+
+template <int MODE>
+int dispatch_chain(const ChainArgs& a, unsigned grid, cudaStream_t st) {
+  switch (a.sub.n) {
+#define HK_CH_CASE(NN) \
+  case NN: k_chain<NN, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    HK_CH_CASE(2)
+    HK_CH_CASE(3)
+    HK_CH_CASE(4)
+    HK_CH_CASE(5)
+    HK_CH_CASE(6)
+    HK_CH_CASE(7)
+    HK_CH_CASE(8)
+#undef HK_CH_CASE
+    default:
+      set_error("decay chain supports 2..%d sub-daughters, got %d", kFastMaxN, a.sub.n);
+      return HK_EUNSUPPORTED;
+  }
+  return check_launch("k_chain");
+}
+
+template <int MODE, int N>
+int dispatch_gen_chain_sub(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
+  switch (a.sub.n) {
+    case 2: k_generate_chain<N, 2, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    case 3: k_generate_chain<N, 3, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    case 4: k_generate_chain<N, 4, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    default:
+      set_error("fused chain supports 2..4 sub-daughters, got %d", a.sub.n);
+      return HK_EUNSUPPORTED;
+  }
+  return check_launch("k_generate_chain");
+}
+
+template <int MODE>
+int dispatch_gen_chain(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
+  switch (a.d.n) {
+    case 2: return dispatch_gen_chain_sub<MODE, 2>(a, grid, st);
+    case 3: return dispatch_gen_chain_sub<MODE, 3>(a, grid, st);
+    case 4: return dispatch_gen_chain_sub<MODE, 4>(a, grid, st);
+    case 5: return dispatch_gen_chain_sub<MODE, 5>(a, grid, st);
+    case 6: return dispatch_gen_chain_sub<MODE, 6>(a, grid, st);
+    default:
+      set_error("fused chain supports 2..6 parent daughters, got %d", a.d.n);
+      return HK_EUNSUPPORTED;
+  }
+}
+
+int validate_decay(const hk_decay_t* d, const char* what) {
+  HK_REQUIRE(d != nullptr, "%s: NULL decay", what);
+  HK_REQUIRE(d->n >= 2 && d->n <= HK_MAX_DAUGHTERS, "%s: daughter count %d outside 2..%d", what,
+             d->n, HK_MAX_DAUGHTERS);
+  return HK_OK;
+}
+
+int validate_key(const hk_key_t* k, const char* what) {
+  HK_REQUIRE(k != nullptr, "%s: NULL key", what);
+  HK_REQUIRE(k->mode == HK_RNG_REFERENCE || k->mode == HK_RNG_PHILOX, "%s: bad rng mode %d", what,
+             k->mode);
+  return HK_OK;
+}
+
+int validate_program(const hk_program_t* f, int n_cols) {
+  HK_REQUIRE(f != nullptr, "NULL program");
+  HK_REQUIRE(f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "program length %d", f->n_ops);
+  HK_REQUIRE(f->result >= 0 && f->result < HK_MAX_SLOTS, "program result slot %d", f->result);
+  for (int i = 0; i < f->n_ops; ++i) {
+    HK_REQUIRE(f->op[i] >= HK_OP_COL && f->op[i] <= HK_OP_SQUARE, "op %d: bad opcode %d", i,
+               f->op[i]);
+    HK_REQUIRE(f->dst[i] >= 0 && f->dst[i] < HK_MAX_SLOTS, "op %d: bad dst", i);
+    if (f->op[i] == HK_OP_COL) {
+      HK_REQUIRE(f->a[i] >= 0 && f->a[i] < n_cols, "op %d: column %d outside 0..%d", i, f->a[i],
+                 n_cols - 1);
+    } else if (f->op[i] != HK_OP_CONST) {
+      HK_REQUIRE(f->a[i] >= 0 && f->a[i] < HK_MAX_SLOTS, "op %d: bad slot a", i);
+      HK_REQUIRE(f->b[i] >= 0 && f->b[i] < HK_MAX_SLOTS, "op %d: bad slot b", i);
+    }
+  }
+  return HK_OK;
+}
+
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int64_t hk_num_chunks(int64_t ev_count) { return num_chunks(ev_count); }
+
+int hk_rng_raw64(const hk_key_t* key, const uint64_t* d_counters, int64_t n, uint64_t* d_out,
+                 void* stream) {
+  if (int rc = validate_key(key, "hk_rng_raw64")) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_counters && d_out, "NULL pointer");
+  k_rng<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(make_rng(*key), d_counters, n,
+                                                                    d_out, nullptr);
+  return check_launch("k_rng");
+}
+
+int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, double* d_out,
+                   void* stream) {
+  if (int rc = validate_key(key, "hk_rng_uniform")) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_counters && d_out, "NULL pointer");
+  k_rng<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(make_rng(*key), d_counters, n,
+                                                                    nullptr, d_out);
+  return check_launch("k_rng");
+}
+
+int hk_phsp_generate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
+                     int64_t ev_count, double* const* d_cols, double* d_wpartials, void* stream) {
+  if (int rc = validate_decay(spec, "hk_phsp_generate")) return rc;
+  if (int rc = validate_key(key, "hk_phsp_generate")) return rc;
+  HK_REQUIRE(ev_count >= 0, "negative ev_count");
+  if (ev_count == 0) return HK_OK;
+  GenArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.d = *spec;
+  a.rp = make_rng(*key);
+  a.ev_begin = ev_begin;
+  a.count = ev_count;
+  a.wpart = d_wpartials;
+  a.store = d_cols != nullptr;
+  if (d_cols) {
+    for (int j = 0; j < 4 * spec->n + 1; ++j) {
+      HK_REQUIRE(d_cols[j] != nullptr, "column %d is NULL", j);
+      a.cols[j] = d_cols[j];
+    }
+  }
+  HK_REQUIRE(a.store || a.wpart, "nothing to write (no columns, no partials)");
+  const unsigned grid = chunk_grid(num_chunks(ev_count));
+  cudaStream_t st = as_stream(stream);
+  return key->mode == HK_RNG_REFERENCE ? dispatch_generate<HK_RNG_REFERENCE>(a, grid, st)
+                                       : dispatch_generate<HK_RNG_PHILOX>(a, grid, st);
+}
+
+int hk_phsp_decay_chain(const double* d_w_in, const double* const* d_p4_in,
+                        const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
+                        int64_t ev_count, double* d_w_out, double* const* d_sub_cols,
+                        uint64_t* d_first_bad, void* stream) {
+  if (int rc = validate_decay(sub, "hk_phsp_decay_chain")) return rc;
+  if (int rc = validate_key(sub_key, "hk_phsp_decay_chain")) return rc;
+  HK_REQUIRE(ev_count >= 0, "negative ev_count");
+  if (ev_count == 0) return HK_OK;
+  HK_REQUIRE(d_w_in && d_p4_in && d_w_out && d_sub_cols, "NULL pointer");
+  ChainArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.sub = *sub;
+  a.rp = make_rng(*sub_key);
+  a.ev_begin = ev_begin;
+  a.count = ev_count;
+  a.w_in = d_w_in;
+  for (int c = 0; c < 4; ++c) {
+    HK_REQUIRE(d_p4_in[c], "input column %d NULL", c);
+    a.p4_in[c] = d_p4_in[c];
+  }
+  a.w_out = d_w_out;
+  for (int j = 0; j < 4 * sub->n; ++j) {
+    HK_REQUIRE(d_sub_cols[j], "sub column %d NULL", j);
+    a.sub_cols[j] = d_sub_cols[j];
+  }
+  a.first_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  const unsigned grid = chunk_grid(num_chunks(ev_count));
+  cudaStream_t st = as_stream(stream);
+  return sub_key->mode == HK_RNG_REFERENCE ? dispatch_chain<HK_RNG_REFERENCE>(a, grid, st)
+                                           : dispatch_chain<HK_RNG_PHILOX>(a, grid, st);
+}
+
+int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t daughter_index,
+                           const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
+                           int64_t ev_count, double* const* d_cols, double* d_wpartials,
+                           uint64_t* d_first_bad, void* stream) {
+  if (int rc = validate_decay(spec, "hk_phsp_generate_chain")) return rc;
+  if (int rc = validate_decay(sub, "hk_phsp_generate_chain")) return rc;
+  if (int rc = validate_key(key, "hk_phsp_generate_chain")) return rc;
+  if (int rc = validate_key(sub_key, "hk_phsp_generate_chain")) return rc;
+  HK_REQUIRE(key->mode == sub_key->mode, "parent and sub-decay keys must share an rng mode");
+  HK_REQUIRE(daughter_index >= 1 && daughter_index <= spec->n, "daughter index %d out of range 1..%d",
+             daughter_index, spec->n);
+  HK_REQUIRE(ev_count >= 0, "negative ev_count");
+  if (ev_count == 0) return HK_OK;
+  HK_REQUIRE(d_cols != nullptr, "NULL columns");
+  const int ncols = 4 * (spec->n - 1 + sub->n) + 1;
+  HK_REQUIRE(ncols <= kMaxCols, "final state too large (%d columns)", ncols);
+  GenChainArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.d = *spec;
+  a.sub = *sub;
+  a.rp = make_rng(*key);
+  a.rp_sub = make_rng(*sub_key);
+  a.k = daughter_index - 1;
+  a.ev_begin = ev_begin;
+  a.count = ev_count;
+  for (int j = 0; j < ncols; ++j) {
+    HK_REQUIRE(d_cols[j], "column %d NULL", j);
+    a.cols[j] = d_cols[j];
+  }
+  a.wpart = d_wpartials;
+  a.first_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  const unsigned grid = chunk_grid(num_chunks(ev_count));
+  cudaStream_t st = as_stream(stream);
+  return key->mode == HK_RNG_REFERENCE ? dispatch_gen_chain<HK_RNG_REFERENCE>(a, grid, st)
+                                       : dispatch_gen_chain<HK_RNG_PHILOX>(a, grid, st);
+}
+
+int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_count,
+                    const hk_program_t* f, double* d_partials, uint64_t* d_first_bad,
+                    void* stream) {
+  HK_REQUIRE(d_cols && n_cols >= 1 && n_cols <= kMaxCols, "bad columns (%d)", n_cols);
+  if (int rc = validate_program(f, n_cols)) return rc;
+  HK_REQUIRE(ev_count >= 0, "negative ev_count");
+  if (ev_count == 0) return HK_OK;
+  HK_REQUIRE(d_partials, "NULL partials");
+  MomArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < n_cols; ++c) {
+    HK_REQUIRE(d_cols[c], "column %d NULL", c);
+    a.cols[c] = d_cols[c];
+  }
+  a.n_cols = n_cols;
+  a.count = ev_count;
+  a.f = *f;
+  a.part = d_partials;
+  // d_first_bad[0] = first zero divisor, d_first_bad[1] = first non-finite f
+  a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  a.nonfinite_bad = d_first_bad ? reinterpret_cast<unsigned long long*>(d_first_bad) + 1 : nullptr;
+  k_moments<<<chunk_grid(num_chunks(ev_count)), kBlock, 0, as_stream(stream)>>>(a);
+  return check_launch("k_moments");
+}
+
+int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const hk_program_t* f,
+                   double* d_out, uint64_t* d_first_bad, void* stream) {
+  HK_REQUIRE(d_cols && n_cols >= 1 && n_cols <= kMaxCols, "bad columns (%d)", n_cols);
+  if (int rc = validate_program(f, n_cols)) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_out, "NULL output");
+  MomArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < n_cols; ++c) {
+    HK_REQUIRE(d_cols[c], "column %d NULL", c);
+    a.cols[c] = d_cols[c];
+  }
+  a.n_cols = n_cols;
+  a.count = n;
+  a.f = *f;
+  a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  k_map<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, as_stream(stream)>>>(a, d_out);
+  return check_launch("k_map");
+}
+
+int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
+                      int64_t ev_count, const hk_program_t* f, double* d_partials,
+                      uint64_t* d_first_bad, void* stream) {
+  if (int rc = validate_decay(spec, "hk_phsp_integrate")) return rc;
+  if (int rc = validate_key(key, "hk_phsp_integrate")) return rc;
+  if (int rc = validate_program(f, 4 * spec->n + 1)) return rc;
+  HK_REQUIRE(ev_count >= 0, "negative ev_count");
+  if (ev_count == 0) return HK_OK;
+  HK_REQUIRE(d_partials, "NULL partials");
+  IntArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.d = *spec;
+  a.rp = make_rng(*key);
+  a.ev_begin = ev_begin;
+  a.count = ev_count;
+  a.f = *f;
+  a.part = d_partials;
+  a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  a.nonfinite_bad = d_first_bad ? reinterpret_cast<unsigned long long*>(d_first_bad) + 1 : nullptr;
+  const unsigned grid = chunk_grid(num_chunks(ev_count));
+  cudaStream_t st = as_stream(stream);
+  return key->mode == HK_RNG_REFERENCE ? dispatch_integrate<HK_RNG_REFERENCE>(a, grid, st)
+                                       : dispatch_integrate<HK_RNG_PHILOX>(a, grid, st);
+}
+
+int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,
+                     void* stream) {
+  HK_REQUIRE(width >= 1 && width <= 32, "fold width %d outside 1..32", width);
+  HK_REQUIRE(n_parts >= 0 && d_out, "bad fold arguments");
+  HK_REQUIRE(n_parts == 0 || d_partials, "NULL partials");
+  return launch_fold(d_partials, n_parts, width, d_out, as_stream(stream));
+}
+
+int hk_unweight_flags(const double* d_w, int64_t n, double w_max, const hk_key_t* key,
+                      uint64_t ev_begin, uint8_t* d_flags, int64_t* d_counts,
+                      uint64_t* d_first_bad, void* stream) {
+  if (int rc = validate_key(key, "hk_unweight_flags")) return rc;
+  HK_REQUIRE(key->mode == HK_RNG_REFERENCE, "unweighting uses the reference stream");
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_w && d_flags && d_counts, "NULL pointer");
+  UnwArgs a;
+  a.w = d_w;
+  a.n = n;
+  a.w_max = w_max;
+  a.rp = make_rng(*key);
+  a.ev_begin = ev_begin;
+  a.flags = d_flags;
+  a.counts = reinterpret_cast<long long*>(d_counts);
+  a.first_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  k_unweight_flags<<<chunk_grid(num_chunks(n)), kBlock, 0, as_stream(stream)>>>(a);
+  return check_launch("k_unweight_flags");
+}
+
+int hk_scan_counts(const int64_t* d_counts, int64_t n, int64_t* d_out, int64_t* d_total,
+                   void* stream) {
+  HK_REQUIRE(n >= 0 && d_total, "bad scan arguments");
+  HK_REQUIRE(n == 0 || (d_counts && d_out), "NULL pointer");
+  k_scan_counts<<<1, 1024, 0, as_stream(stream)>>>(reinterpret_cast<const long long*>(d_counts), n,
+                                                   reinterpret_cast<long long*>(d_out),
+                                                   reinterpret_cast<long long*>(d_total));
+  return check_launch("k_scan_counts");
+}
+
+int hk_compact(const double* const* d_in, int32_t n_cols, int64_t n, const uint8_t* d_flags,
+               const int64_t* d_offsets, double* const* d_out, int32_t weight_col, void* stream) {
+  HK_REQUIRE(n_cols >= 1 && n_cols <= kMaxCols, "bad column count %d", n_cols);
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_in && d_out && d_flags && d_offsets, "NULL pointer");
+  CompactArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < n_cols; ++c) {
+    HK_REQUIRE(d_in[c] && d_out[c], "column %d NULL", c);
+    a.in[c] = d_in[c];
+    a.out[c] = d_out[c];
+  }
+  a.n_cols = n_cols;
+  a.weight_col = weight_col;
+  a.n = n;
+  a.flags = d_flags;
+  a.offsets = reinterpret_cast<const long long*>(d_offsets);
+  k_compact<<<chunk_grid(num_chunks(n)), kBlock, 0, as_stream(stream)>>>(a);
+  return check_launch("k_compact");
+}
+
+}  // extern "C"

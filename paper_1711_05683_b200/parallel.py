@@ -1,0 +1,112 @@
+"""Deterministic data parallelism across GPUs (reference parallel.py:1-92).
+
+The reference splits every bulk operation into fixed 65 536-row batches and
+4096-row chunk partials folded in a fixed order, so results do not depend on
+the worker count.  Here the "workers" are GPUs, one process per GPU
+(torch.distributed, NCCL over NVLink/NVSwitch):
+
+* events shard as contiguous, chunk-aligned global row ranges
+  (``shard_range``); each rank generates/evaluates its range with the
+  *global* row index, so shards are bit-identical to the same rows of a
+  one-GPU run (RNG counters are global, phasespace.py:105-109);
+* the only exchange is the chunk partials: ``gather_partials`` all-gathers
+  them (a few KB per rank) into global chunk order and every rank folds the
+  same array with the same fixed tree -- so the reduced value is bitwise
+  independent of the number of GPUs (the analogue of the reference's
+  worker-invariance tests, test_phasespace.py:87-93, test_fitting.py:120-124).
+"""
+
+from __future__ import annotations
+
+import os
+
+from . import _lib
+
+CHUNK = _lib.HK_CHUNK          # parallel.py:18
+EVAL_BATCH = 16 * CHUNK        # parallel.py:21
+
+
+def resolve_workers(workers: int | None) -> int:
+    """Reference knob (parallel.py:42-48); accepted and ignored by the GPU path."""
+    if workers is None or workers == 0:
+        return os.cpu_count() or 1
+    if workers < 0:
+        raise ValueError(f"workers must be >= 0, got {workers}")
+    return workers
+
+
+def batch_ranges(n: int, batch: int = EVAL_BATCH) -> list[tuple[int, int]]:
+    return [(s, min(s + batch, n)) for s in range(0, n, batch)]
+
+
+def chunk_bounds(start: int, stop: int, chunk: int = CHUNK) -> list[tuple[int, int]]:
+    first = (start // chunk) * chunk
+    return [(max(s, start), min(s + chunk, stop)) for s in range(first, stop, chunk)
+            if max(s, start) < min(s + chunk, stop)]
+
+
+def shard_range(n: int, rank: int, world: int, chunk: int = CHUNK) -> tuple[int, int]:
+    """Contiguous chunk-aligned [a, b) of rank's rows; shards cover [0, n)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    nch = (n + chunk - 1) // chunk
+    c0 = nch * rank // world
+    c1 = nch * (rank + 1) // world
+    return min(c0 * chunk, n), min(c1 * chunk, n)
+
+
+def dist_info(group=None) -> tuple[int, int]:
+    """(rank, world) of the default process group, (0, 1) when not initialised."""
+    torch = _lib.torch()
+    dist = torch.distributed
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def gather_partials(local, n_total: int, width: int, group=None):
+    """All-gather per-chunk partials (local: flat tensor of this rank's chunks
+    x width) into global chunk order on every rank.
+
+    Shards are chunk-aligned, so the concatenation of the ranks' partials in
+    rank order is exactly the global chunk sequence.  Unequal shard sizes are
+    padded to the largest and trimmed after the gather.
+    """
+    torch = _lib.torch()
+    rank, world = dist_info(group)
+    if world == 1:
+        return local
+    dist = torch.distributed
+    nch = (n_total + CHUNK - 1) // CHUNK
+    sizes = [(nch * (r + 1) // world - nch * r // world) for r in range(world)]
+    cap = max(sizes) * width
+    buf = torch.zeros(cap, dtype=local.dtype, device=local.device)
+    buf[: local.numel()] = local
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[: s * width] for o, s in zip(out, sizes)])
+
+
+def sharded_weight_moments(block_shard, n_total: int, group=None):
+    """Global (sum w, sum w^2) of a sharded generation: gather + same fold."""
+    parts = block_shard.meta["weight_partials"]
+    full = gather_partials(parts, n_total, 2, group)
+    return _lib.fold(full, (n_total + CHUNK - 1) // CHUNK, 2)
+
+
+def sharded_integrate(expr, spec, mother, n_total: int, key, arg_builder, group=None,
+                      rng: str = "reference"):
+    """phsp_integrate over n_total events sharded across the process group
+    (config C5 at 1/2/4/8 GPUs); returns the IntegrationResult on every rank."""
+    from .phasespace import _finish_average, phsp_integrate  # noqa: PLC0415
+
+    rank, world = dist_info(group)
+    a, b = shard_range(n_total, rank, world)
+    if b > a:
+        parts = phsp_integrate(expr, spec, mother, b - a, key, arg_builder, rng=rng,
+                               row_offset=a, return_partials=True)
+    else:
+        parts = _lib.empty(0)
+    full = gather_partials(parts, n_total, 5, group)
+    tot = _lib.fold(full, (n_total + CHUNK - 1) // CHUNK, 5)
+    return _finish_average(tot.cpu().numpy(), n_total)

@@ -1,0 +1,250 @@
+"""CPU tests: the C ABI surface, host-side logic, and program lowering
+(checked with a numpy emulation of the device interpreter against the oracle)."""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.common import B0_DAUGHTERS, B0_MASS, m12sq_builder, m23sq_builder, run_program_numpy
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions() -> set[str]:
+    text = open(os.path.join(ROOT, "include", "hepkit_cuda.h")).read()
+    return set(re.findall(r"^(?:int|int64_t)\s+(hk_\w+)\(", text, flags=re.M))
+
+
+def test_library_exports_every_declared_symbol(hk):
+    from paper_1711_05683_b200 import _lib
+    lib = _lib.load_library()
+    declared = _header_functions()
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.hk_abi_version() == 1
+    assert lib.hk_num_chunks(0) == 0
+    assert lib.hk_num_chunks(4096) == 1
+    assert lib.hk_num_chunks(4097) == 2
+    assert lib.hk_num_chunks(10**10) == (10**10 + 4095) // 4096
+
+
+def test_struct_layouts_match_header(hk):
+    from paper_1711_05683_b200 import _lib
+    # hk_decay_t: 2 ints + 2 doubles + 2*16 doubles + 4 + 1 doubles
+    assert ctypes.sizeof(_lib.hk_decay_t) == 8 + 16 + 8 * 32 + 8 * 5
+    assert ctypes.sizeof(_lib.hk_key_t) == 32
+    assert ctypes.sizeof(_lib.hk_program_t) == 8 + 4 * 4 * 48 + 8 * 2 * 48
+    assert ctypes.sizeof(_lib.hk_model_t) == 8 + 4 * 8 + 8 * 4 * 8
+
+
+def test_no_device_fails_loudly(hk):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    with pytest.raises(hk.DeviceUnavailable):
+        hk.phsp_generate(hk.DecaySpec(1.0, (0.1, 0.2)), hk.FourVector.at_rest(1.0), 10, hk.RngKey(1, 1))
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1711_05683_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("Oracle", ""), f
+
+
+class TestHostKinematics:
+    def test_breakup_known_answers(self, hk, golden):
+        _, s = golden
+        assert hk.breakup_momentum(2.0, 0.5, 0.3) == s["kat"]["breakup_2_05_03"] == 0.9119210492142398
+        assert hk.breakup_momentum(1.0, 0.5, 0.5) == 0.0
+        assert hk.breakup_momentum(1.0, 0.0, 0.0) == 0.5
+        with pytest.raises(hk.BelowThreshold):
+            hk.breakup_momentum(0.9, 0.5, 0.5)
+
+    def test_max_weight_matches_reference(self, hk, golden):
+        _, s = golden
+        for b in s["gen_blocks"]:
+            assert hk.phsp_max_weight(hk.DecaySpec(b["M"], tuple(b["masses"]))) == b["max_weight"]
+
+    def test_decay_spec_validation(self, hk):
+        with pytest.raises(hk.BelowThreshold):
+            hk.DecaySpec(1.0, (0.5, 0.5))
+        with pytest.raises(ValueError):
+            hk.DecaySpec(1.0, (0.5,))
+        with pytest.raises(ValueError):
+            hk.DecaySpec(1.0, (0.5, -0.1))
+
+    def test_boost_into_z(self, hk):
+        beta = 0.6
+        g = 1 / math.sqrt(1 - beta * beta)
+        v = hk.boost_into(hk.FourVector(1.0, 0.0, 0.0, 0.0), hk.FourVector(g, 0.0, 0.0, g * beta))
+        assert v.e == pytest.approx(g, rel=1e-15)
+        assert v.pz == pytest.approx(g * beta, rel=1e-15)
+
+    def test_schema(self, hk):
+        assert hk.phsp_schema(2).names == ("weight", "p1_e", "p1_px", "p1_py", "p1_pz",
+                                           "p2_e", "p2_px", "p2_py", "p2_pz")
+
+
+class TestLowering:
+    """Lowered programs, run by a numpy emulation of the kernel interpreter,
+    reproduce the reference integrands on oracle blocks."""
+
+    def _block(self, oracle, n=20_000):
+        return oracle.generate(B0_DAUGHTERS, B0_MASS, n, 5, 1)
+
+    def test_pair_mass_identity_bit_exact(self, hk, oracle):
+        from paper_1711_05683_b200.functors import lower_average
+        blk = self._block(oracle)
+        names = hk.phsp_schema(3).names
+        prog, _ = lower_average(hk.identity(), m12sq_builder, names)
+        f, div0 = run_program_numpy(prog, [blk[n] for n in names])
+        assert np.array_equal(f, oracle.pair_mass2(blk, 1, 2) + 0.0)
+        assert not div0.any()
+
+    def test_breit_wigner_builtin(self, hk, oracle):
+        from paper_1711_05683_b200.functors import lower_average
+        blk = self._block(oracle)
+        names = hk.phsp_schema(3).names
+        prog, _ = lower_average(hk.breit_wigner(0.89555, 0.0473), m23sq_builder, names)
+        f, _ = run_program_numpy(prog, [blk[n] for n in names])
+        ref = oracle.breit_wigner(oracle.pair_mass2(blk, 2, 3), 0.89555, 0.0473)
+        assert np.array_equal(f, ref)
+
+    def test_algebra_and_composition(self, hk, oracle):
+        from paper_1711_05683_b200.functors import lower_average
+        blk = self._block(oracle, 5000)
+        names = hk.phsp_schema(3).names
+        mu, s, tau = hk.Parameter("mu", 10.0), hk.Parameter("s", 2.0), hk.Parameter("tau", 3.0)
+        g = hk.shape_gaussian(mu, s)
+        e = hk.shape_exponential(tau)
+        expr = hk.compose(g + e * hk.identity(), [hk.identity()]) / (hk.identity() + hk.constant(1.0))
+        prog, _ = lower_average(expr, m12sq_builder, names)
+        f, _ = run_program_numpy(prog, [blk[n] for n in names])
+        x = oracle.pair_mass2(blk, 1, 2)
+        ref = expr.eval((x,))
+        assert np.array_equal(f, ref)
+
+    def test_closure_tracing(self, hk, oracle):
+        from paper_1711_05683_b200.functors import lower_average
+        blk = self._block(oracle, 3000)
+        names = hk.phsp_schema(3).names
+        clo = hk.wrap_closure(lambda x, p: np.sqrt(x[0]) * 2.0 + x[0] ** 2 - np.log(x[0]))
+        prog, _ = lower_average(clo, m12sq_builder, names)
+        f, _ = run_program_numpy(prog, [blk[n] for n in names])
+        x = oracle.pair_mass2(blk, 1, 2) + 0.0
+        assert np.array_equal(f, np.sqrt(x) * 2.0 + x ** 2 - np.log(x))
+
+    def test_untraceable_raises(self, hk):
+        from paper_1711_05683_b200.functors import lower_average
+        names = hk.phsp_schema(3).names
+        bad = hk.wrap_closure(lambda x, p: np.where(x[0] > 1, 1.0, 0.0))
+        with pytest.raises(NotImplementedError):
+            lower_average(bad, m12sq_builder, names)
+        with pytest.raises(NotImplementedError):
+            lower_average(hk.identity(), lambda cols: (np.sin(cols["p1_e"]),), names)
+
+    def test_program_register_budget(self, hk):
+        from paper_1711_05683_b200.functors import compile_program
+        node = ("col", 0)
+        for k in range(1, 20):     # long dependent chain: needs 2 live slots
+            node = ("add", node, ("col", k % 13))
+        prog = compile_program(node)
+        assert max(prog.dst[i] for i in range(prog.n_ops)) < 4
+
+
+class TestHostFit:
+    def test_minimize_quadratic(self, hk):
+        a = hk.Parameter("a", 0.0, step=0.5)
+        res = hk.minimize(lambda ps: (ps["a"].value - 3.0) ** 2, hk.ParamSet([a]))
+        assert res.status is hk.FitStatus.CONVERGED
+        assert a.value == pytest.approx(3.0, abs=1e-4)
+        assert res.errors["a"] == pytest.approx(0.7071067811865475, rel=1e-4)
+
+    def test_constant_shift_invariance(self, hk):
+        base = lambda ps: (ps["a"].value - 2.0) ** 4 + (ps["a"].value + 1.0) ** 2  # noqa: E731
+        a1 = hk.Parameter("a", 0.3, step=0.4)
+        r1 = hk.minimize(base, hk.ParamSet([a1]))
+        a2 = hk.Parameter("a", 0.3, step=0.4)
+        r2 = hk.minimize(lambda ps: base(ps) + 4.0, hk.ParamSet([a2]))
+        assert a2.value == a1.value and r2.nll_min == r1.nll_min + 4.0
+
+    def test_bounded_and_fixed(self, hk):
+        obj = lambda ps: (ps["a"].value - 1.5) ** 2 + 0.7  # noqa: E731
+        free = hk.Parameter("a", 0.2, step=0.3)
+        rf = hk.minimize(obj, hk.ParamSet([free]))
+        bnd = hk.Parameter("a", 0.2, step=0.3, lower=-5.0, upper=5.0)
+        rb = hk.minimize(obj, hk.ParamSet([bnd]))
+        assert bnd.value == pytest.approx(free.value, abs=5e-4)
+        assert rb.nll_min == pytest.approx(rf.nll_min, abs=1e-7)
+        b = hk.Parameter("b", 2.5, fixed=True)
+        hk.minimize(lambda ps: (ps["a"].value - 1.0) ** 2 + ps["b"].value,
+                    hk.ParamSet([hk.Parameter("a", 0.0, step=0.5), b]))
+        assert b.value == 2.5
+
+    def test_rosenbrock_and_max_iterations(self, hk):
+        x, y = hk.Parameter("x", -1.0, step=0.2), hk.Parameter("y", 1.5, step=0.2)
+        res = hk.minimize(lambda ps: (1 - ps["x"].value) ** 2 + 5.0 * (ps["y"].value - ps["x"].value ** 2) ** 2,
+                          hk.ParamSet([x, y]), max_iterations=5000)
+        assert res.status is hk.FitStatus.CONVERGED
+        assert x.value == pytest.approx(1.0, abs=1e-3) and y.value == pytest.approx(1.0, abs=1e-3)
+        a = hk.Parameter("a", 100.0, step=0.001)
+        r = hk.minimize(lambda ps: abs(ps["a"].value), hk.ParamSet([a]), max_iterations=3)
+        assert r.status is hk.FitStatus.MAX_ITERATIONS and r.errors is None
+
+    def test_numeric_errors_correlated(self, hk):
+        H = np.array([[2.0, 0.6], [0.6, 1.0]])
+        ps = hk.ParamSet([hk.Parameter("x", 0.0), hk.Parameter("y", 0.0)])
+        err = hk.numeric_errors(lambda p: 0.5 * float(np.array([p["x"].value, p["y"].value]) @ H
+                                                      @ np.array([p["x"].value, p["y"].value])), ps)
+        cov = np.linalg.inv(H)
+        assert err["x"] == pytest.approx(math.sqrt(cov[0, 0]), rel=1e-5)
+        assert hk.numeric_errors(lambda p: -p["x"].value ** 2, hk.ParamSet([hk.Parameter("x", 0.0)])) is None
+
+    def test_norms(self, hk):
+        e = hk.shape_exponential(hk.Parameter("tau", 1.0))
+        pdf = hk.make_pdf(e, hk.exponential_norm(e), hk.BoundedRegion(((0.0, 10.0),)))
+        assert pdf.norm() == pytest.approx(0.9999546000702375, rel=1e-14)
+        g = hk.shape_gaussian(hk.Parameter("m", 0.0), hk.Parameter("s", 1.0))
+        pg = hk.make_pdf(g, hk.gaussian_norm(g), hk.BoundedRegion(((-10.0, 10.0),)))
+        assert pg.value((0.0,)) == pytest.approx(0.3989422804014327, rel=1e-13)
+        for _ in range(3):
+            pg.value((1.0,))
+        assert pg.norm_computations == 1
+
+
+class TestStoreAndSharding:
+    def test_store_host_ops(self, hk, tmp_path):
+        s = hk.ColumnStore(hk.ColumnSchema.real64("a", "b"))
+        for i in range(10):
+            s.push((float(i), float(i * i)))
+        assert len(s) == 10 and s.row(3) == (3.0, 9.0)
+        sel = s.where_mask(np.arange(10) % 3 == 0)
+        assert sel.column("a").tolist() == [0.0, 3.0, 6.0, 9.0]
+        p = tmp_path / "x.csv"
+        s.write_csv(str(p))
+        back = hk.read_csv(str(p))
+        assert np.array_equal(back.column("b"), s.column("b"))
+        with pytest.raises(ValueError):
+            hk.ColumnSchema.real64("a", "a")
+
+    def test_shard_ranges_cover_and_align(self):
+        from paper_1711_05683_b200.parallel import CHUNK, shard_range
+        for n in (0, 1, 4095, 4096, 4097, 10**6, 10**8 + 17):
+            for world in (1, 2, 3, 4, 8):
+                rs = [shard_range(n, r, world) for r in range(world)]
+                assert rs[0][0] == 0 and rs[-1][1] == n
+                for (a0, b0), (a1, _) in zip(rs, rs[1:]):
+                    assert b0 == a1
+                for a, b in rs:
+                    assert a % CHUNK == 0 and a <= b
