@@ -84,29 +84,37 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64
 _I32 = ctypes.c_int32
+_D = ctypes.POINTER(hk_decay_t)      # structs: ctypes passes byref automatically
+_K = ctypes.POINTER(hk_key_t)
+_F = ctypes.POINTER(hk_program_t)
+_M = ctypes.POINTER(hk_model_t)
+_PP = ctypes.POINTER(ctypes.c_void_p)  # double* const* column-pointer arrays
+_PD = ctypes.POINTER(ctypes.c_double)  # host doubles
+_PU = ctypes.POINTER(ctypes.c_uint64)  # host u64
+_INT = ctypes.c_int
 _SIGS = {
-    "hk_abi_version": (ctypes.c_int, []),
-    "hk_last_error": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t]),
-    "hk_device_info": (ctypes.c_int, [_P, _P]),
+    "hk_abi_version": (_INT, []),
+    "hk_last_error": (_INT, [ctypes.c_char_p, ctypes.c_size_t]),
+    "hk_device_info": (_INT, [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "hk_num_chunks": (_I64, [_I64]),
-    "hk_rng_raw64": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
-    "hk_rng_uniform": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
-    "hk_phsp_generate": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P]),
-    "hk_phsp_generate_host": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P, ctypes.c_size_t, _P]),
-    "hk_phsp_decay_chain": (ctypes.c_int, [_P, _P, _P, _P, _U64, _I64, _P, _P, _P, _P]),
-    "hk_phsp_generate_chain": (ctypes.c_int, [_P, _P, _I32, _P, _P, _U64, _I64, _P, _P, _P, _P]),
-    "hk_phsp_moments": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _P]),
-    "hk_phsp_integrate": (ctypes.c_int, [_P, _P, _U64, _I64, _P, _P, _P, _P]),
-    "hk_map_program": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _P]),
-    "hk_fold_partials": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
-    "hk_nll_partials": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
-    "hk_nll_eval": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
-    "hk_model_density": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
-    "hk_yield_partials": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P]),
-    "hk_unweight_flags": (ctypes.c_int, [_P, _I64, ctypes.c_double, _P, _U64, _P, _P, _P, _P]),
-    "hk_compact": (ctypes.c_int, [_P, _I32, _I64, _P, _P, _P, _I32, _P]),
-    "hk_scan_counts": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
-    "hk_sample_pdf": (ctypes.c_int, [_P, _I32, _P, _P, ctypes.c_double, _P, _U64, _I64, _I32, _P, _P, _P]),
+    "hk_rng_raw64": (_INT, [_K, _P, _I64, _P, _P]),
+    "hk_rng_uniform": (_INT, [_K, _P, _I64, _P, _P]),
+    "hk_phsp_generate": (_INT, [_D, _K, _U64, _I64, _PP, _P, _P]),
+    "hk_phsp_generate_host": (_INT, [_D, _K, _U64, _I64, _PP, _PD, _P, ctypes.c_size_t, _P]),
+    "hk_phsp_decay_chain": (_INT, [_P, _PP, _D, _K, _U64, _I64, _P, _PP, _P, _P]),
+    "hk_phsp_generate_chain": (_INT, [_D, _K, _I32, _D, _K, _U64, _I64, _PP, _P, _P, _P]),
+    "hk_phsp_moments": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),
+    "hk_phsp_integrate": (_INT, [_D, _K, _U64, _I64, _F, _P, _P, _P]),
+    "hk_map_program": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),
+    "hk_fold_partials": (_INT, [_P, _I64, _I32, _P, _P]),
+    "hk_nll_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
+    "hk_nll_eval": (_INT, [_P, _I64, _M, _P, _PD, _PU, _P]),
+    "hk_model_density": (_INT, [_P, _I64, _M, _P, _P]),
+    "hk_yield_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
+    "hk_unweight_flags": (_INT, [_P, _I64, ctypes.c_double, _K, _U64, _P, _P, _P, _P]),
+    "hk_compact": (_INT, [_PP, _I32, _I64, _P, _P, _PP, _I32, _P]),
+    "hk_scan_counts": (_INT, [_P, _I64, _P, _P, _P]),
+    "hk_sample_pdf": (_INT, [_F, _I32, _PD, _PD, ctypes.c_double, _K, _U64, _I64, _I32, _PP, _P, _P]),
 }
 
 _lock = threading.Lock()

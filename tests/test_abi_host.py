@@ -36,6 +36,52 @@ def test_library_exports_every_declared_symbol(hk):
     assert lib.hk_num_chunks(10**10) == (10**10 + 4095) // 4096
 
 
+def test_every_entry_point_marshals_and_validates(hk):
+    """Call each C entry point through the ctypes signatures with empty work
+    (validation runs, no kernel is launched) -- catches ABI drift on the CPU."""
+    from paper_1711_05683_b200 import _lib
+    L = _lib.load_library()
+    spec = hk.DecaySpec(5.27966, (3.0969, 0.493677, 0.13957039))
+    d = _lib.make_decay(spec)
+    k = _lib.make_key(hk.RngKey(1, 1))
+    cols = (ctypes.c_void_p * 65)(*([1] * 65))
+    prog = hk.functors.compile_program(("add", ("col", 1), ("const", 2.0)))
+    model = _lib.hk_model_t()
+    model.n_comp, model.kind[0], model.yield_[0], model.norm[0], model.p0[0], model.p1[0] = 1, 0, 1.0, 1.0, 0.0, 1.0
+    dummy = ctypes.create_string_buffer(1 << 16)
+    dp = ctypes.addressof(dummy)
+    two = (ctypes.c_double * 2)()
+    OK = _lib.HK_OK
+    assert L.hk_rng_raw64(k, None, 0, None, None) == OK
+    assert L.hk_rng_uniform(k, None, 0, None, None) == OK
+    assert L.hk_phsp_generate(d, k, 0, 0, cols, None, None) == OK
+    assert L.hk_phsp_generate_host(d, k, 0, 0, cols, two, dp, len(dummy), None) == OK
+    assert L.hk_phsp_decay_chain(dp, cols, d, k, 0, 0, dp, cols, None, None) == OK
+    assert L.hk_phsp_generate_chain(d, k, 1, d, k, 0, 0, cols, None, None, None) == OK
+    assert L.hk_phsp_moments(cols, 13, 0, prog, dp, None, None) == OK
+    assert L.hk_phsp_integrate(d, k, 0, 0, prog, dp, None, None) == OK
+    assert L.hk_map_program(cols, 13, 0, prog, dp, None, None) == OK
+    assert L.hk_nll_partials(dp, 0, model, dp, None, None) == OK
+    assert L.hk_model_density(dp, 0, model, dp, None) == OK
+    assert L.hk_yield_partials(dp, 0, model, dp, None, None) == OK
+    assert L.hk_unweight_flags(dp, 0, 1.0, k, 0, dp, dp, None, None) == OK
+    assert L.hk_compact(cols, 13, 0, dp, dp, cols, 0, None) == OK
+    lo = (ctypes.c_double * 1)(0.0)
+    assert L.hk_sample_pdf(prog, 1, lo, lo, 1.0, k, 0, 0, 10, cols, dp, None) == OK
+    # validation errors come back as HK_EINVAL with a message
+    assert L.hk_nll_eval(dp, 0, model, dp, two, ctypes.byref(ctypes.c_uint64()), None) == _lib.HK_EINVAL
+    assert "empty" in _lib.last_error()
+    bad = _lib.make_decay(spec)
+    bad.n = 1
+    assert L.hk_phsp_generate(bad, k, 0, 10, cols, None, None) == _lib.HK_EINVAL
+    assert "daughter count" in _lib.last_error()
+    with pytest.raises(ValueError):
+        _lib.check(L.hk_phsp_generate(bad, k, 0, 10, cols, None, None), "generate")
+    nd, sm = ctypes.c_int(-1), ctypes.c_int(-1)
+    assert L.hk_device_info(ctypes.byref(nd), ctypes.byref(sm)) == OK
+    assert nd.value >= 0
+
+
 def test_struct_layouts_match_header(hk):
     from paper_1711_05683_b200 import _lib
     # hk_decay_t: 2 ints + 2 doubles + 2*16 doubles + 4 + 1 doubles
