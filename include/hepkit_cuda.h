@@ -191,10 +191,28 @@ int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_coun
 int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const hk_program_t* f,
                    double* d_out, uint64_t* d_first_bad, void* stream);
 
-/* Fused generate -> f -> moments with no event store (config C5). */
+/* Dalitz-plane integrands with a specialised (non-interpreted) device path:
+ * s = m^2 of daughters i+j (0-based) in the op order of the reference's
+ * pinned integrand (test_phasespace.py:196-201); f = s + 0.0 (identity) or a
+ * Breit-Wigner 1/((s - m0^2)^2 + m0^2 g0^2).  The host recognises these
+ * structurally in a lowered expression. */
+#define HK_PAIR_NONE 0
+#define HK_PAIR_MASS2 1
+#define HK_PAIR_BW 2
+typedef struct hk_pair_integrand {
+  int32_t kind;
+  int32_t i;
+  int32_t j;
+  int32_t _pad;
+  double m0;
+  double g0;
+} hk_pair_integrand_t;
+
+/* Fused generate -> f -> moments with no event store (config C5).  f is the
+ * program, or `pair` (non-NULL, kind != HK_PAIR_NONE) selects the fast path. */
 int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
-                      int64_t ev_count, const hk_program_t* f, double* d_partials,
-                      uint64_t* d_first_bad, void* stream);
+                      int64_t ev_count, const hk_program_t* f, const hk_pair_integrand_t* pair,
+                      double* d_partials, uint64_t* d_first_bad, void* stream);
 
 /* Deterministic fold of n_parts partials of `width` (<= 32) doubles each
  * (parallel.py:86-92 semantics, fixed tree order) into d_out[width]. */
@@ -209,7 +227,10 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
 
 /* One FCN evaluation end to end: partials + fold + 16-byte readback.
  * Synchronous.  *h_logsum = sum_e ln density; *h_first_bad = first failing
- * row or HK_NO_BAD_ROW.  d_work needs hk_num_chunks(n) + 2 doubles. */
+ * row or HK_NO_BAD_ROW.  One kernel launch (the last CTA folds the chunk
+ * partials in a fixed order) plus one 16-byte readback.  d_work needs
+ * hk_num_chunks(n) + 4 doubles, ZERO-FILLED before its first use; the kernel
+ * re-arms it for the next call. */
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
 

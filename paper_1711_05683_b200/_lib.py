@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhepkit_cuda.so")
+LIB_PATH = os.environ.get("HK_LIB_PATH") or os.path.join(HERE, "libhepkit_cuda.so")
 
 HK_OK, HK_EINVAL, HK_ECUDA, HK_EDOMAIN, HK_EUNSUPPORTED = 0, 1, 2, 3, 4
 HK_CHUNK = 4096
@@ -80,6 +80,14 @@ class hk_model_t(ctypes.Structure):
                 ("p1", ctypes.c_double * HK_MAX_COMPONENTS)]
 
 
+HK_PAIR_NONE, HK_PAIR_MASS2, HK_PAIR_BW = 0, 1, 2
+
+
+class hk_pair_integrand_t(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("i", ctypes.c_int32), ("j", ctypes.c_int32),
+                ("_pad", ctypes.c_int32), ("m0", ctypes.c_double), ("g0", ctypes.c_double)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _U64 = ctypes.c_uint64
@@ -104,7 +112,7 @@ _SIGS = {
     "hk_phsp_decay_chain": (_INT, [_P, _PP, _D, _K, _U64, _I64, _P, _PP, _P, _P]),
     "hk_phsp_generate_chain": (_INT, [_D, _K, _I32, _D, _K, _U64, _I64, _PP, _P, _P, _P]),
     "hk_phsp_moments": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),
-    "hk_phsp_integrate": (_INT, [_D, _K, _U64, _I64, _F, _P, _P, _P]),
+    "hk_phsp_integrate": (_INT, [_D, _K, _U64, _I64, _F, ctypes.POINTER(hk_pair_integrand_t), _P, _P, _P]),
     "hk_map_program": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),
     "hk_fold_partials": (_INT, [_P, _I64, _I32, _P, _P]),
     "hk_nll_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
@@ -167,17 +175,27 @@ def torch():
     return _torch
 
 
+_device_ok = False
+
+
+def _require_device() -> None:
+    global _device_ok
+    if not _device_ok:
+        if not torch().cuda.is_available():
+            raise DeviceUnavailable("no CUDA device is visible; the hot path has no CPU fallback")
+        load_library()
+        _device_ok = True
+
+
 def device():
     """The current CUDA device; raises when there is none (no CPU fallback)."""
+    _require_device()
     t = torch()
-    if not t.cuda.is_available():
-        raise DeviceUnavailable("no CUDA device is visible; the hot path has no CPU fallback")
-    load_library()
     return t.device("cuda", t.cuda.current_device())
 
 
 def lib() -> ctypes.CDLL:
-    device()
+    _require_device()
     return _lib
 
 

@@ -87,6 +87,68 @@ __global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, in
   }
 }
 
+// One-launch FCN: the same event pass, then the last CTA to finish folds all
+// chunk partials in a fixed order (deterministic whichever CTA is last),
+// publishes (sum, first bad row) and re-arms the workspace for the next call.
+// The first-bad cell holds ~row under atomicMax so that an all-zero
+// workspace means "no bad row".
+struct FcnWork {
+  double* out;               // [0] sum of logs, [1] first bad row (u64 bits)
+  unsigned long long* bad;   // ~row of the first non-positive density, 0 = none
+  unsigned int* ticket;      // CTAs finished
+  double* part;              // one partial per chunk
+};
+
+template <bool GE>
+__global__ void __launch_bounds__(kBlock) k_nll_fused(const double* __restrict__ x, int64_t n,
+                                                      const __grid_constant__ Coeffs c, FcnWork w) {
+  const int64_t chunks = (n + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    double acc[1] = {0.0};
+    const int64_t r0 = ch * HK_CHUNK + threadIdx.x;
+    unsigned long long bad = 0;
+    if (ch * HK_CHUNK + HK_CHUNK <= n) {
+      double xv[kRowsPerThread];
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const double d = GE ? density_ge(c, xv[i]) : density(c, xv[i]);
+        if (!(d > 0.0) || !isfinite(d)) bad = max(bad, ~(unsigned long long)(r0 + i * kBlock));
+        acc[0] += log(d);
+      }
+    } else {
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const int64_t r = r0 + i * kBlock;
+        if (r < n) {
+          const double d = GE ? density_ge(c, __ldg(x + r)) : density(c, __ldg(x + r));
+          if (!(d > 0.0) || !isfinite(d)) bad = max(bad, ~(unsigned long long)r);
+          acc[0] += log(d);
+        }
+      }
+    }
+    if (bad) atomicMax(w.bad, bad);
+    block_sum_store<1>(acc, w.part + ch);
+  }
+  __shared__ unsigned int s_ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(w.ticket, 1u);
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  __threadfence();
+  double acc[1] = {0.0};
+  for (int64_t i = threadIdx.x; i < chunks; i += kBlock) acc[0] += __ldcg(w.part + i);
+  __shared__ double total;
+  block_sum_store<1>(acc, &total);
+  if (threadIdx.x == 0) {
+    const unsigned long long b = atomicExch(w.bad, 0ull);
+    w.out[0] = total;
+    w.out[1] = __longlong_as_double((long long)~b);
+    *w.ticket = 0u;
+  }
+}
+
 // Reference op order (fitting.py:160-166, functors.py:142-143, :161) with no
 // contraction -- used only for the value quoted in the error message.
 __global__ void k_density_exact(const double* x, int64_t n, const __grid_constant__ hk_model_t m,
@@ -229,14 +291,20 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
   HK_REQUIRE(d_x && d_work && h_logsum && h_first_bad, "NULL pointer");
   cudaStream_t st = as_stream(stream);
-  const int64_t chunks = num_chunks(n);
-  // d_work layout: [0] fold output, [1] first-bad cell (u64), [2..] partials
-  double* out = d_work;
-  unsigned long long* bad = reinterpret_cast<unsigned long long*>(d_work + 1);
-  double* part = d_work + 2;
-  HK_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
-  if (int rc = launch_nll(d_x, n, c, part, bad, st)) return rc;
-  if (int rc = launch_fold(part, chunks, 1, out, st)) return rc;
+  // d_work layout (zero-filled once by the caller, re-armed by the kernel):
+  // [0] sum of logs, [1] first bad row, [2] ~bad-row cell, [3] CTA ticket, [4..] partials
+  FcnWork w;
+  w.out = d_work;
+  w.bad = reinterpret_cast<unsigned long long*>(d_work + 2);
+  w.ticket = reinterpret_cast<unsigned int*>(d_work + 3);
+  w.part = d_work + 4;
+  const unsigned grid = chunk_grid(num_chunks(n));
+  const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
+  if (ge)
+    k_nll_fused<true><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
+  else
+    k_nll_fused<false><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
+  if (int rc = check_launch("k_nll_fused")) return rc;
   thread_local Readback rb;
   if (!rb.h) HK_CUDA(cudaMallocHost(&rb.h, 2 * sizeof(double)));
   HK_CUDA(cudaMemcpyAsync(rb.h, d_work, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));

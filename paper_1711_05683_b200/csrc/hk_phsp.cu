@@ -20,6 +20,14 @@ namespace hk {
 constexpr int kMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
 constexpr int kFastMaxN = 8;  // templated register-resident kernels for n <= 8
 
+// CTAs per SM the generator is register-budgeted for: 3 (<= 80 registers)
+// measured best for n <= 4 (2.41 vs 2.55 ms per 1e8 3-body events at 2);
+// larger final states spill heavily at 80 registers and keep 2.
+template <int N>
+struct GenMinBlocks {
+  static constexpr int value = N <= 4 ? 3 : 2;
+};
+
 struct GenArgs {
   hk_decay_t d;
   RngParams rp;
@@ -32,7 +40,8 @@ struct GenArgs {
 
 // ------------------------------------------------------------ generation ---
 template <int N, int MODE>
-__global__ void __launch_bounds__(kBlock) k_generate(const __grid_constant__ GenArgs a) {
+__global__ void __launch_bounds__(kBlock, GenMinBlocks<N>::value)
+    k_generate(const __grid_constant__ GenArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
@@ -47,7 +56,7 @@ __global__ void __launch_bounds__(kBlock) k_generate(const __grid_constant__ Gen
         const double w = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r, p);
         if (a.d.moving) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
         }
         if (a.store) {
           __stcs(a.cols[0] + r, w);
@@ -100,12 +109,40 @@ struct IntArgs {
   double* part;  // 5 doubles per chunk
   unsigned long long* div0_bad;
   unsigned long long* nonfinite_bad;
+  hk_pair_integrand_t pair;  // kind != HK_PAIR_NONE: f from the fast pair-mass path
 };
+
+// daughter q's component c of the register-resident event, q a runtime index
+template <int N>
+__device__ __forceinline__ double pick(const double (&p)[4 * N], int q, int c) {
+  double v = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) v = (j == q) ? p[4 * j + c] : v;
+  return v;
+}
+
+// m^2 of daughters i+j with the op order of the reference's pinned integrand
+// (test_phasespace.py:196-201), then identity (+0.0) or a Breit-Wigner.
+template <int N>
+__device__ __forceinline__ double pair_integrand(const double (&p)[4 * N],
+                                                 const hk_pair_integrand_t& f) {
+  const double e = pick<N>(p, f.i, 0) + pick<N>(p, f.j, 0);
+  const double x = pick<N>(p, f.i, 1) + pick<N>(p, f.j, 1);
+  const double y = pick<N>(p, f.i, 2) + pick<N>(p, f.j, 2);
+  const double z = pick<N>(p, f.i, 3) + pick<N>(p, f.j, 3);
+  const double s = e * e - x * x - y * y - z * z;
+  if (f.kind == HK_PAIR_BW) {
+    const double t = s - f.m0 * f.m0;
+    return 1.0 / (t * t + (f.m0 * f.m0) * (f.g0 * f.g0));
+  }
+  return s + 0.0;
+}
 
 // phsp_generate -> phsp_average (phasespace.py:162-188 then :310-349) with the
 // event kept in registers: 0 bytes of HBM per event.
-template <int N, int MODE>
-__global__ void __launch_bounds__(kBlock) k_integrate(const __grid_constant__ IntArgs a) {
+template <int N, int MODE, bool PAIR>
+__global__ void __launch_bounds__(kBlock, PAIR ? GenMinBlocks<N>::value : 1)
+    k_integrate(const __grid_constant__ IntArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
@@ -122,14 +159,19 @@ __global__ void __launch_bounds__(kBlock) k_integrate(const __grid_constant__ In
         const double w = rest_event<N, MODE>(a.d, a.rp, row, p);
         if (a.d.moving) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
         }
-        v[0] = w;
+        double f;
+        if (PAIR) {
+          f = pair_integrand<N>(p, a.pair);
+        } else {
+          v[0] = w;
 #pragma unroll
-        for (int j = 0; j < 4 * N; ++j) v[1 + j] = p[j];
-        bool div0 = false;
-        const double f = run_program(a.f, [&](int col) { return v[col]; }, &div0);
-        if (div0) record_bad(a.div0_bad, row);
+          for (int j = 0; j < 4 * N; ++j) v[1 + j] = p[j];
+          bool div0 = false;
+          f = run_program(a.f, [&](int col) { return v[col]; }, &div0);
+          if (div0) record_bad(a.div0_bad, row);
+        }
         if (!isfinite(f)) record_bad(a.nonfinite_bad, row);
         const double ww = w * w;
         acc[0] += w;
@@ -227,9 +269,9 @@ __global__ void __launch_bounds__(kBlock) k_chain(const __grid_constant__ ChainA
       if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
       double q[4 * NS];
       const double ws = rest_event<NS, MODE>(a.sub, a.rp, row, q);
-      const Frame f = make_frame(fe, fx, fy, fz, fm);
+      const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
 #pragma unroll
-      for (int s = 0; s < NS; ++s) boost(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+      for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
       __stcs(a.w_out + r, __ldg(a.w_in + r) * ws);
 #pragma unroll
       for (int j = 0; j < 4 * NS; ++j) __stcs(a.sub_cols[j] + r, q[j]);
@@ -269,7 +311,7 @@ __global__ void __launch_bounds__(kBlock) k_generate_chain(const __grid_constant
         const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
         if (a.d.moving) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) boost(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+          for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
         }
         double fe = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
 #pragma unroll
@@ -285,9 +327,9 @@ __global__ void __launch_bounds__(kBlock) k_generate_chain(const __grid_constant
         if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
         double q[4 * NS];
         const double ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
-        const Frame f = make_frame(fe, fx, fy, fz, fm);
+        const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
 #pragma unroll
-        for (int s = 0; s < NS; ++s) boost(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+        for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
         const double w = wp * ws;
         __stcs(a.cols[0] + r, w);
 #pragma unroll
@@ -486,8 +528,13 @@ int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
 template <int MODE>
 int dispatch_integrate(const IntArgs& a, unsigned grid, cudaStream_t st) {
   switch (a.d.n) {
-#define HK_INT_CASE(NN) \
-  case NN: k_integrate<NN, MODE><<<grid, kBlock, 0, st>>>(a); break;
+#define HK_INT_CASE(NN)                                                  \
+  case NN:                                                               \
+    if (a.pair.kind != HK_PAIR_NONE)                                     \
+      k_integrate<NN, MODE, true><<<grid, kBlock, 0, st>>>(a);           \
+    else                                                                 \
+      k_integrate<NN, MODE, false><<<grid, kBlock, 0, st>>>(a);          \
+    break;
     HK_INT_CASE(2)
     HK_INT_CASE(3)
     HK_INT_CASE(4)
@@ -756,11 +803,19 @@ int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const
 }
 
 int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
-                      int64_t ev_count, const hk_program_t* f, double* d_partials,
-                      uint64_t* d_first_bad, void* stream) {
+                      int64_t ev_count, const hk_program_t* f, const hk_pair_integrand_t* pair,
+                      double* d_partials, uint64_t* d_first_bad, void* stream) {
   if (int rc = validate_decay(spec, "hk_phsp_integrate")) return rc;
   if (int rc = validate_key(key, "hk_phsp_integrate")) return rc;
-  if (int rc = validate_program(f, 4 * spec->n + 1)) return rc;
+  const bool fast = pair && pair->kind != HK_PAIR_NONE;
+  if (fast) {
+    HK_REQUIRE(pair->kind == HK_PAIR_MASS2 || pair->kind == HK_PAIR_BW, "bad pair kind %d",
+               pair->kind);
+    HK_REQUIRE(pair->i >= 0 && pair->j >= 0 && pair->i < spec->n && pair->j < spec->n,
+               "pair (%d, %d) outside the %d daughters", pair->i, pair->j, spec->n);
+  } else if (int rc = validate_program(f, 4 * spec->n + 1)) {
+    return rc;
+  }
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
   if (ev_count == 0) return HK_OK;
   HK_REQUIRE(d_partials, "NULL partials");
@@ -770,7 +825,10 @@ int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_b
   a.rp = make_rng(*key);
   a.ev_begin = ev_begin;
   a.count = ev_count;
-  a.f = *f;
+  if (fast)
+    a.pair = *pair;
+  else
+    a.f = *f;
   a.part = d_partials;
   a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
   a.nonfinite_bad = d_first_bad ? reinterpret_cast<unsigned long long*>(d_first_bad) + 1 : nullptr;

@@ -554,13 +554,46 @@ def compile_program(root) -> "_lib.hk_program_t":
     return prog
 
 
-def lower_average(expr: FunctorExpr, arg_builder, names: Sequence[str]):
+def lower_average(expr: FunctorExpr, arg_builder, names: Sequence[str], with_root: bool = False):
     """Program computing expr(*arg_builder(columns)) per event, plus the
-    argument nodes (for error messages)."""
+    argument nodes (for error messages) [and the IR root]."""
     args = trace_arg_builder(arg_builder, names)
     if len(args) != expr.arity:
         raise EvaluationError(f"expression consumes {expr.arity} arguments, got {len(args)}")
-    return compile_program(expr.lower(args)), args
+    root = expr.lower(args)
+    if with_root:
+        return compile_program(root), args, root
+    return compile_program(root), args
+
+
+def pair_mass2_node(i: int, j: int):
+    """IR of m^2(daughters i+j) (1-based) exactly as tracing the reference's
+    pinned builder produces it (test_phasespace.py:196-201)."""
+    def comp(c):
+        return ("add", ("col", 1 + 4 * (i - 1) + c), ("col", 1 + 4 * (j - 1) + c))
+
+    e, x, y, z = (comp(c) for c in range(4))
+    return ("sub", ("sub", ("sub", ("mul", e, e), ("mul", x, x)), ("mul", y, y)), ("mul", z, z))
+
+
+def match_pair_integrand(root, n_daughters: int):
+    """hk_pair_integrand_t if `root` is m^2_ij + 0.0 or BW(m^2_ij), else None."""
+    kind, inner = None, None
+    if root[0] == "add0":
+        kind, inner = _lib.HK_PAIR_MASS2, root[1]
+    elif root[0] == "bw":
+        kind, inner = _lib.HK_PAIR_BW, root[1]
+    if kind is None or inner[0] != "sub":
+        return None
+    for i in range(1, n_daughters + 1):
+        for j in range(1, n_daughters + 1):
+            if i != j and inner == pair_mass2_node(i, j):
+                out = _lib.hk_pair_integrand_t()
+                out.kind, out.i, out.j = kind, i - 1, j - 1
+                if kind == _lib.HK_PAIR_BW:
+                    out.m0, out.g0 = root[2], root[3]
+                return out
+    return None
 
 
 def eval_node(node, cols: dict[int, float]) -> float:

@@ -27,7 +27,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .functors import EvaluationError, FunctorExpr, columns_used, eval_node, lower_average
+from .functors import (EvaluationError, FunctorExpr, columns_used, eval_node, lower_average,
+                       match_pair_integrand)
 from .integrate import IntegrationResult
 from .kinematics import MASS_TOLERANCE, BelowThreshold, FourVector, breakup_momentum, invariant_mass
 from .rng import RngKey, rng_mode
@@ -279,12 +280,13 @@ def phsp_integrate(expr: FunctorExpr, spec: DecaySpec, mother: FourVector, n_eve
     if n_events == 0:
         raise ValueError("cannot average over an empty block")
     names = phsp_schema(spec.n).names
-    prog, args = lower_average(expr, arg_builder, names)
+    prog, args, root = lower_average(expr, arg_builder, names, with_root=True)
+    pair = match_pair_integrand(root, spec.n)     # Dalitz m^2_ij / BW(m^2_ij): specialised path
     d = _lib.make_decay(spec, mother, m_mother)
     k = _lib.make_key(key, rng_mode(rng))
     bad = _lib.bad_cells(2)
     parts = _lib.empty(5 * _lib.num_chunks(n_events))
-    _lib.check(_lib.lib().hk_phsp_integrate(d, k, _lib.u64(row_offset), n_events, prog,
+    _lib.check(_lib.lib().hk_phsp_integrate(d, k, _lib.u64(row_offset), n_events, prog, pair,
                                             _lib.ptr(parts), _lib.ptr(bad), _lib.stream_ptr()),
                "hk_phsp_integrate")
     flags = _lib.read_bad(bad)

@@ -59,7 +59,11 @@ def test_every_entry_point_marshals_and_validates(hk):
     assert L.hk_phsp_decay_chain(dp, cols, d, k, 0, 0, dp, cols, None, None) == OK
     assert L.hk_phsp_generate_chain(d, k, 1, d, k, 0, 0, cols, None, None, None) == OK
     assert L.hk_phsp_moments(cols, 13, 0, prog, dp, None, None) == OK
-    assert L.hk_phsp_integrate(d, k, 0, 0, prog, dp, None, None) == OK
+    assert L.hk_phsp_integrate(d, k, 0, 0, prog, None, dp, None, None) == OK
+    pair = _lib.hk_pair_integrand_t(_lib.HK_PAIR_BW, 1, 2, 0, 0.89555, 0.0473)
+    assert L.hk_phsp_integrate(d, k, 0, 0, None, pair, dp, None, None) == OK
+    pair.i = 5
+    assert L.hk_phsp_integrate(d, k, 0, 10, None, pair, dp, None, None) == _lib.HK_EINVAL
     assert L.hk_map_program(cols, 13, 0, prog, dp, None, None) == OK
     assert L.hk_nll_partials(dp, 0, model, dp, None, None) == OK
     assert L.hk_model_density(dp, 0, model, dp, None) == OK
@@ -199,6 +203,22 @@ class TestLowering:
             lower_average(bad, m12sq_builder, names)
         with pytest.raises(NotImplementedError):
             lower_average(hk.identity(), lambda cols: (np.sin(cols["p1_e"]),), names)
+
+    def test_pair_integrand_recognition(self, hk):
+        from paper_1711_05683_b200 import _lib
+        from paper_1711_05683_b200.functors import lower_average, match_pair_integrand
+        names = hk.phsp_schema(3).names
+        _, _, root = lower_average(hk.identity(), m12sq_builder, names, with_root=True)
+        p = match_pair_integrand(root, 3)
+        assert p is not None and (p.kind, p.i, p.j) == (_lib.HK_PAIR_MASS2, 0, 1)
+        _, _, root = lower_average(hk.breit_wigner(0.89555, 0.0473), m23sq_builder, names, with_root=True)
+        p = match_pair_integrand(root, 3)
+        assert (p.kind, p.i, p.j, p.m0, p.g0) == (_lib.HK_PAIR_BW, 1, 2, 0.89555, 0.0473)
+        # anything else stays on the generic interpreter
+        _, _, root = lower_average(hk.identity() * hk.identity(), m12sq_builder, names, with_root=True)
+        assert match_pair_integrand(root, 3) is None
+        _, _, root = lower_average(hk.identity(), lambda c: (c["p1_e"] * c["p2_e"],), names, with_root=True)
+        assert match_pair_integrand(root, 3) is None
 
     def test_program_register_budget(self, hk):
         from paper_1711_05683_b200.functors import compile_program

@@ -250,7 +250,9 @@ def test_fused_integrate_equals_stored_average(cuda, hk):
     spec, mother = _b0(hk)
     n = 1_000_000
     blk = hk.phsp_generate(spec, mother, n, hk.RngKey(1, 1))
-    for expr, builder in ((hk.identity(), m12sq_builder), (hk.breit_wigner(0.89555, 0.0473), m23sq_builder)):
+    for expr, builder in ((hk.identity(), m12sq_builder),                     # pair fast path
+                          (hk.breit_wigner(0.89555, 0.0473), m23sq_builder),  # pair fast path
+                          (hk.identity() * hk.identity(), m12sq_builder)):    # interpreter
         a = hk.phsp_average(expr, blk, builder)
         b = hk.phsp_integrate(expr, spec, mother, n, hk.RngKey(1, 1), builder)
         assert b.value == pytest.approx(a.value, rel=1e-10)

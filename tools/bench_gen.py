@@ -1,0 +1,62 @@
+"""Micro-benchmark of the generator kernel through the C ABI (HK_LIB_PATH selects a build).
+
+    HK_LIB_PATH=... python tools/bench_gen.py [--n 1e8] [--reps 10] [--rng reference]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1711_05683_b200 as hk  # noqa: E402
+from paper_1711_05683_b200 import _lib  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=float, default=1e8)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--rng", default="reference")
+    ap.add_argument("--check", action="store_true")
+    a = ap.parse_args()
+    n = int(a.n)
+    M, ms = 5.27966, (3.0969, 0.493677, 0.13957039)
+    spec = hk.DecaySpec(M, ms)
+    d = _lib.make_decay(spec)
+    k = _lib.make_key(hk.RngKey(1, 1), hk.rng.rng_mode(a.rng))
+    cols = [_lib.empty(n) for _ in range(13)]
+    cp = _lib.ptr_array(cols)
+    wp = _lib.empty(2 * _lib.num_chunks(n))
+    st = torch.cuda.current_stream()
+    L = _lib.lib()
+    for _ in range(3):
+        _lib.check(L.hk_phsp_generate(d, k, 0, n, cp, _lib.ptr(wp), st.cuda_stream), "gen")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        L.hk_phsp_generate(d, k, 0, n, cp, _lib.ptr(wp), st.cuda_stream)
+    e1.record()
+    e1.synchronize()
+    ms_ = e0.elapsed_time(e1) / a.reps
+    out = {"lib": os.environ.get("HK_LIB_PATH", "default"), "n": n, "ms": ms_, "ev_per_s": n / ms_ * 1e3,
+           "GBps": 104 * n / ms_ / 1e6}
+    if a.check:
+        from oracle import oracle as O
+        ref = O.generate(ms, M, 200_000, 1, 1, threads=8)
+        worst = 0.0
+        for j in range(3):
+            e = np.abs(ref[f"p{j+1}_e"])
+            for c in ("e", "px", "py", "pz"):
+                g = cols[1 + 4 * j + "e px py pz".split().index(c)][:200_000].cpu().numpy()
+                worst = max(worst, float(np.max(np.abs(g - ref[f"p{j+1}_{c}"]) / e)))
+        out["max_dc_over_E"] = worst
+        out["weights_bit_exact"] = bool(np.array_equal(cols[0][:200_000].cpu().numpy(), ref["weight"]))
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
