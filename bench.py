@@ -189,8 +189,20 @@ def fcn_bench(hk, torch, evals: int = 200) -> dict:
     ev1.record(st)
     ev1.synchronize()
     kt = ev0.elapsed_time(ev1) / evals * 1e-3
+    # the one-launch C-ABI FCN call alone (kernel + 16-byte readback + sync), no Python model lowering
+    work = torch.zeros(_lib.num_chunks(FCN_EVENTS) + 4, dtype=torch.float64, device=x.device)
+    logsum, first = ctypes.c_double(), ctypes.c_uint64()
+    for _ in range(3):
+        _lib.lib().hk_nll_eval(_lib.ptr(x), FCN_EVENTS, lm, _lib.ptr(work), ctypes.byref(logsum),
+                               ctypes.byref(first), st.cuda_stream)
+    c0 = time.perf_counter()
+    for _ in range(evals):
+        _lib.lib().hk_nll_eval(_lib.ptr(x), FCN_EVENTS, lm, _lib.ptr(work), ctypes.byref(logsum),
+                               ctypes.byref(first), st.cuda_stream)
+    ct = (time.perf_counter() - c0) / evals
     return {"metric": "FCN evals/s @1e7 events (gauss+exp extended NLL, fp64)", "value": 1.0 / dt,
             "unit": "evals/s", "us_per_eval": dt * 1e6, "kernel_us_per_eval": kt * 1e6,
+            "c_abi_us_per_eval": ct * 1e6,
             "kernel_events_per_s": FCN_EVENTS / kt, "evals": evals,
             "data": "1e7 events from generate_model_sample(build_model(scale=200), RngKey(7,2), poisson=False) on device"}
 
