@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "hepkit_cuda.h"
+#include "hk_math.cuh"
 
 namespace hk {
 
@@ -181,13 +182,33 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
+// ~1 ulp square root for x >= 0 without the IEEE slow-path branch: MUFU
+// rsqrt seed, one Newton step on 1/sqrt, then a residual-corrected product.
+// 0, inf and NaN pass through unchanged (as IEEE sqrt returns them); x < 0
+// is never passed (callers clamp with max0 or add squares) and subnormal x
+// (< 2.2e-308 GeV^2, physically impossible here) would also pass through.
+// Used for energies and |sin theta|, never for the breakup momenta that
+// make up the weight.
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x * y, y, 1.5);  // 1/sqrt(x) to ~2^-45
+  const double s = x * y;
+  const double r = fma(-s, s, x);
+  const double out = fma(r, 0.5 * y, s);
+  return (x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308) ? out : x;
+}
+
 // Boost frame with one reciprocal for the three beta components and one for
-// gamma^2/(gamma+1); gamma itself stays an IEEE division so a massless frame
-// (fm = 0) gives exactly the reference's inf.
+// gamma^2/(gamma+1).  gamma = fe/fm: a reciprocal for fm > 0, the IEEE
+// division otherwise, so a massless frame (fm = 0) gives the reference's inf.
 __device__ __forceinline__ Frame make_frame_fast(double fe, double fx, double fy, double fz,
                                                  double fm) {
   Frame f;
-  f.gamma = fe / fm;
+  // branch-free: fm == +0 selects fe * inf, which is IEEE fe / +0 (inf, -inf
+  // or NaN), so the scheduler can interleave across frames
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  f.gamma = fm == 0.0 ? fe * inf : fe * fast_rcp(fm);
   const double r = fast_rcp(fe);
   f.bx = fx * r;
   f.by = fy * r;
@@ -260,12 +281,12 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
     // phi = 2 pi u: sincospi(2u) needs no Payne-Hanek reduction and differs
     // from cos(fl(2 pi u)) by at most the rounding of fl(2 pi u) (<= 4.4e-16)
     const double two_u = 2.0 * to_unit(bits[N - 2 + 2 * (k - 1) + 1]);
-    const double sz = sqrt(max0(1.0 - cz * cz));  // cancellation-sensitive: no FMA
+    const double sz = fast_sqrt(max0(1.0 - cz * cz));  // cancellation-sensitive: no FMA
     double sn, cs;
-    sincospi(two_u, &sn, &cs);
+    math::k_sincospi(two_u, &sn, &cs);
     const double nx = sz * cs, ny = sz * sn, nz = cz;
     const double clm = inv[k - 1];
-    const double cle = sqrt(q * q + clm * clm);
+    const double cle = fast_sqrt(q * q + clm * clm);
     const double clx = q * nx, cly = q * ny, clz = q * nz;
     const Frame f = make_frame_fast(cle, clx, cly, clz, clm);
     if (k == 1) {
@@ -274,7 +295,7 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
 #pragma unroll
       for (int j = 0; j < k; ++j) boost_fma(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
     }
-    p[4 * k + 0] = sqrt(q * q + d.masses[k] * d.masses[k]);
+    p[4 * k + 0] = fast_sqrt(q * q + d.masses[k] * d.masses[k]);
     p[4 * k + 1] = -clx;
     p[4 * k + 2] = -cly;
     p[4 * k + 3] = -clz;

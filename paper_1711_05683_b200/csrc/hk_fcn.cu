@@ -36,9 +36,9 @@ __device__ __forceinline__ double density(const Coeffs& c, double x) {
     double t;
     if (c.kind[k] == HK_SHAPE_GAUSS) {
       const double z = (x - c.shift[k]) * c.scale[k];
-      t = c.amp[k] * exp(-0.5 * z * z);
+      t = c.amp[k] * math::k_exp(-0.5 * z * z);
     } else {
-      t = c.amp[k] * exp(x * c.scale[k]);
+      t = c.amp[k] * math::k_exp(x * c.scale[k]);
     }
     d = k == 0 ? t : d + t;
   }
@@ -49,7 +49,7 @@ __device__ __forceinline__ double density(const Coeffs& c, double x) {
 // cli.py:316-320 / toymodel.py): no component loop, no kind branches.
 __device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
   const double z = (x - c.shift[0]) * c.scale[0];
-  return c.amp[0] * exp(-0.5 * z * z) + c.amp[1] * exp(x * c.scale[1]);
+  return c.amp[0] * math::k_exp(-0.5 * z * z) + c.amp[1] * math::k_exp(x * c.scale[1]);
 }
 
 // sum_e ln d_e as ln(prod_e d_e), the product kept as a mantissa in [1, 2^16)
@@ -134,6 +134,10 @@ struct FcnWork {
   unsigned long long* bad;   // ~row of the first non-positive density, 0 = none
   unsigned int* ticket;      // CTAs finished
   double* part;              // one partial per chunk
+  // optional zero-copy publication into mapped pinned host memory:
+  // host_mail[1..2] = out[0..1], then host_mail[0] = seq (after a system fence)
+  volatile unsigned long long* host_mail;
+  unsigned long long seq;
 };
 
 template <bool GE>
@@ -162,6 +166,12 @@ __global__ void __launch_bounds__(kBlock) k_nll_fused(const double* __restrict__
     w.out[0] = total;
     w.out[1] = __longlong_as_double((long long)~b);
     *w.ticket = 0u;
+    if (w.host_mail) {
+      w.host_mail[1] = (unsigned long long)__double_as_longlong(total);
+      w.host_mail[2] = ~b;
+      __threadfence_system();
+      w.host_mail[0] = w.seq;
+    }
   }
 }
 
@@ -275,13 +285,34 @@ int launch_nll(const double* d_x, int64_t n, const Coeffs& c, double* part,
   return check_launch("k_nll");
 }
 
-// small pinned readback cell per host thread for hk_nll_eval
-struct Readback {
-  double* h = nullptr;
-  ~Readback() {
-    if (h) cudaFreeHost(h);
-  }
+// Mapped pinned mailbox per (host thread, device) for hk_nll_eval:
+// [0] sequence number, [1] sum-of-logs bits, [2] first bad row.
+struct Mailbox {
+  volatile unsigned long long* h = nullptr;  // host view
+  unsigned long long* d = nullptr;           // device view of the same memory
+  unsigned long long seq = 0;
+  int device = -1;
 };
+
+int mailbox(Mailbox** out) {
+  thread_local Mailbox boxes[16];
+  int dev = 0;
+  HK_CUDA(cudaGetDevice(&dev));
+  Mailbox& m = boxes[dev & 15];
+  if (m.device != dev) {
+    void* p = nullptr;
+    HK_CUDA(cudaHostAlloc(&p, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
+    std::memset(p, 0, 4 * sizeof(unsigned long long));
+    void* dp = nullptr;
+    HK_CUDA(cudaHostGetDevicePointer(&dp, p, 0));
+    m.h = static_cast<volatile unsigned long long*>(p);
+    m.d = static_cast<unsigned long long*>(dp);
+    m.seq = 0;
+    m.device = dev;
+  }
+  *out = &m;
+  return HK_OK;
+}
 
 }  // namespace hk
 
@@ -314,6 +345,10 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   w.bad = reinterpret_cast<unsigned long long*>(d_work + 2);
   w.ticket = reinterpret_cast<unsigned int*>(d_work + 3);
   w.part = d_work + 4;
+  Mailbox* mb = nullptr;
+  if (int rc = mailbox(&mb)) return rc;
+  w.host_mail = mb->d;
+  w.seq = ++mb->seq;
   const unsigned grid = chunk_grid(num_chunks(n));
   const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
   if (ge)
@@ -321,12 +356,24 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   else
     k_nll_fused<false><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
   if (int rc = check_launch("k_nll_fused")) return rc;
-  thread_local Readback rb;
-  if (!rb.h) HK_CUDA(cudaMallocHost(&rb.h, 2 * sizeof(double)));
-  HK_CUDA(cudaMemcpyAsync(rb.h, d_work, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  HK_CUDA(cudaStreamSynchronize(st));
-  *h_logsum = rb.h[0];
-  std::memcpy(h_first_bad, &rb.h[1], sizeof(uint64_t));
+  // The last CTA writes the result into mapped host memory and then the
+  // sequence number; spin on it (no memcpy, no stream sync on the fast path).
+  // Every 4096 polls the stream is queried so a faulted kernel cannot hang us.
+  for (unsigned spins = 1;; ++spins) {
+    if (mb->h[0] == w.seq) break;
+    if ((spins & 4095u) == 0) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) {
+        if (mb->h[0] == w.seq) break;
+        set_error("hk_nll_eval: kernel finished without publishing its result");
+        return HK_ECUDA;
+      }
+      if (q != cudaErrorNotReady) return cuda_fail(q, "hk_nll_eval");
+    }
+  }
+  const unsigned long long sum_bits = mb->h[1];
+  std::memcpy(h_logsum, &sum_bits, sizeof(double));
+  *h_first_bad = mb->h[2];
   return HK_OK;
 }
 

@@ -20,9 +20,21 @@ namespace hk {
 constexpr int kMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
 constexpr int kFastMaxN = 8;  // templated register-resident kernels for n <= 8
 
-// CTAs per SM the generator is register-budgeted for: 3 (<= 80 registers)
-// measured best for n <= 4 (2.41 vs 2.55 ms per 1e8 3-body events at 2);
-// larger final states spill heavily at 80 registers and keep 2.
+// Generator shape, measured on B200 for 1e8 3-body events (tools/bench_gen.py):
+//   1 event/iteration, 2 CTAs/SM (<=128 regs) ........ 2.55 ms
+//   1 event/iteration, 3 CTAs/SM (<=80 regs) ......... 2.315 ms
+//   2 events/iteration, 2 CTAs/SM (<=128 regs) ....... 2.240 ms  <- n <= 4
+//   2 events/iteration, 1 CTA/SM ..................... 2.747 ms
+// Two independent events per iteration give the scheduler interleavable
+// dependency chains (the kernel is issue/FP64-latency bound, "wait" stalls);
+// larger final states would spill and keep one event per iteration.
+template <int N>
+struct GenShape {
+  static constexpr int ilp = N <= 4 ? 2 : 1;
+  static constexpr int min_blocks = 2;
+};
+
+// fused integration (no stores), one event per iteration: 3 CTAs/SM for n <= 4
 template <int N>
 struct GenMinBlocks {
   static constexpr int value = N <= 4 ? 3 : 2;
@@ -40,7 +52,7 @@ struct GenArgs {
 
 // ------------------------------------------------------------ generation ---
 template <int N, int MODE>
-__global__ void __launch_bounds__(kBlock, GenMinBlocks<N>::value)
+__global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
     k_generate(const __grid_constant__ GenArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
@@ -48,6 +60,32 @@ __global__ void __launch_bounds__(kBlock, GenMinBlocks<N>::value)
                                   a.d.m_mother);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
+    // full chunks, mother at rest: rows r and r + 2048 together (ILP 2)
+    if (GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
+#pragma unroll 1
+      for (int i = 0; i < kRowsPerThread / 2; ++i) {
+        const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
+        const int64_t r1 = r0 + HK_CHUNK / 2;
+        double p0[4 * N], p1[4 * N];
+        const double w0 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r0, p0);
+        const double w1 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r1, p1);
+        if (a.store) {
+          __stcs(a.cols[0] + r0, w0);
+          __stcs(a.cols[0] + r1, w1);
+#pragma unroll
+          for (int j = 0; j < 4 * N; ++j) {
+            __stcs(a.cols[1 + j] + r0, p0[j]);
+            __stcs(a.cols[1 + j] + r1, p1[j]);
+          }
+        }
+        acc[0] += w0;
+        acc[1] += w0 * w0;
+        acc[0] += w1;
+        acc[1] += w1 * w1;
+      }
+      if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+      continue;
+    }
 #pragma unroll 1
     for (int i = 0; i < kRowsPerThread; ++i) {
       const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;

@@ -44,6 +44,32 @@ def main():
     ms_ = e0.elapsed_time(e1) / a.reps
     out = {"lib": os.environ.get("HK_LIB_PATH", "default"), "n": n, "ms": ms_, "ev_per_s": n / ms_ * 1e3,
            "GBps": 104 * n / ms_ / 1e6}
+    # FCN kernel on 1e7 gauss+exp events (hk_nll_partials, one launch per eval)
+    rs = np.random.default_rng(7)
+    xs = np.clip(np.concatenate([rs.normal(5.0, 0.5, 4_000_000), rs.exponential(3.0, 6_000_000)]), 1e-3, 9.999)
+    x = torch.from_numpy(xs).cuda()
+    from paper_1711_05683_b200.fitting import lower_model
+    g = hk.shape_gaussian(hk.Parameter("mean", 5.0), hk.Parameter("sigma", 0.5))
+    e = hk.shape_exponential(hk.Parameter("tau", 3.0))
+    reg = hk.BoundedRegion(((0.0, 10.0),))
+    model = hk.add_pdfs([hk.Parameter("n_sig", 4e6), hk.Parameter("n_bkg", 6e6)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), reg), hk.make_pdf(e, hk.exponential_norm(e), reg)])
+    lm = lower_model(model)
+    parts = _lib.empty(_lib.num_chunks(x.numel()))
+    bad = _lib.bad_cells(1)
+    for _ in range(3):
+        L.hk_nll_partials(_lib.ptr(x), x.numel(), lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+    e0.record()
+    for _ in range(50):
+        L.hk_nll_partials(_lib.ptr(x), x.numel(), lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+    e1.record()
+    e1.synchronize()
+    out["fcn_kernel_us"] = e0.elapsed_time(e1) / 50 * 1e3
+    if a.check:
+        from oracle import oracle as O
+        want = O.nll(xs, O.gauss_exp_components(5.0, 0.5, 3.0, 4e6, 6e6))
+        got = hk.nll(model, hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [xs]), ["x0"])
+        out["fcn_rel_err"] = abs(got - want) / abs(want)
     if a.check:
         from oracle import oracle as O
         ref = O.generate(ms, M, 200_000, 1, 1, threads=8)
