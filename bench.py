@@ -207,6 +207,90 @@ def fcn_bench(hk, torch, evals: int = 200) -> dict:
             "data": "1e7 events from generate_model_sample(build_model(scale=200), RngKey(7,2), poisson=False) on device"}
 
 
+def _timed(torch, fn, reps: int, dist=None) -> float:
+    """Seconds per call: CUDA events on the current stream, max over ranks."""
+    st = torch.cuda.current_stream()
+    fn()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    e1.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3 / reps
+    if dist:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return dt
+
+
+def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
+    """The other BASELINE.json configs, measured the same way (secondary lines):
+    C1 1e5 generation through the API; C3 fused chain, 1e9 events sharded
+    (1.25e8 per GPU: 1e9/8); C5 fused Dalitz integration of 1e10 events
+    split over the GPUs (strong scaling)."""
+    from paper_1711_05683_b200.parallel import gather_partials, shard_range
+
+    spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
+    out = {}
+    # C1: a small block through the public API (launch + fold bound at this size)
+    n1 = 100_000
+
+    def c1():
+        blk = hk.phsp_generate(spec, mother, n1, hk.RngKey(1, 1), row_offset=rank * n1)
+        return blk.meta["weight_partials"]
+
+    dt = _timed(torch, c1, 50, dist)
+    out["C1"] = {"workload": "1e5 B0->J/psi K pi events per GPU, phsp_generate API (device store)",
+                 "value": world * n1 / dt, "unit": "events/s", "ms_per_call": dt * 1e3}
+    # C3: fused generate + J/psi -> mu mu chain, 4-body final state, 136 B/event
+    n3 = 125_000_000
+    sub = hk.DecaySpec(3.0969, (0.1056583755, 0.1056583755))
+
+    def c3():
+        return hk.phsp_generate_chain(spec, mother, n3, hk.RngKey(1, 1), 1, sub, hk.RngKey(2, 1),
+                                      row_offset=rank * n3)
+
+    c3()
+    torch.cuda.empty_cache()
+    dt = _timed(torch, c3, 5, dist)
+    peak = _peaks()["hbm_gbs"]
+    out["C3"] = {"workload": "B0->J/psi(->mu mu) K pi fused chain, 1.25e8 events per GPU (1e9 / 8), 17 columns",
+                 "value": world * n3 / dt, "unit": "events/s", "ms_per_step": dt * 1e3,
+                 "hbm_GBps_per_gpu": 136 * n3 / dt / 1e9, "frac_of_measured_copy_bw": 136 * n3 / dt / 1e9 / peak}
+    torch.cuda.empty_cache()
+    # C5: 1e10 events, generation -> m^2_12 -> moments, no store; shards + NCCL gather + fold
+
+    def m12(cols):
+        e = cols["p1_e"] + cols["p2_e"]
+        px = cols["p1_px"] + cols["p2_px"]
+        py = cols["p1_py"] + cols["p2_py"]
+        pz = cols["p1_pz"] + cols["p2_pz"]
+        return (e * e - px * px - py * py - pz * pz,)
+
+    n5 = 10_000_000_000
+    a, b = shard_range(n5, rank, world)
+    res = {}
+
+    def c5():
+        parts = hk.phsp_integrate(hk.identity(), spec, mother, b - a, hk.RngKey(1, 1), m12,
+                                  row_offset=a, return_partials=True)
+        full = gather_partials(parts, n5, 5)
+        res["tot"] = _lib.fold(full, _lib.num_chunks(n5), 5)
+
+    dt = _timed(torch, c5, 2, dist)
+    tot = res["tot"].cpu().numpy()
+    mu = tot[1] / tot[0]
+    out["C5"] = {"workload": "1e10 B0->J/psi K pi events, fused generation + <m12^2> weighted average, "
+                             f"strong scaling over {world} GPU(s), no event store",
+                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu)}
+    return out
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -298,6 +382,7 @@ def run_ours(args) -> None:
             e2e["value"] = n_total / float(tt.item())
         del host
 
+    others = None if args.no_configs else other_configs(hk, torch, _lib, rank, world, dist)
     fcn = None
     if rank == 0 and not args.no_fcn:
         fcn = fcn_bench(hk, torch, evals=args.fcn_evals)
@@ -326,6 +411,7 @@ def run_ours(args) -> None:
             "gpu_launches": 2 * args.steps,
             "cpu_baseline": cpu,
             "fcn": fcn,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -342,6 +428,7 @@ def main() -> None:
     ap.add_argument("--no-fcn", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fcn-evals", type=int, default=200)
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C3/C5 secondary measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -238,6 +238,15 @@ __device__ __forceinline__ void boost_rest(const Frame& f, double m, double& e, 
   pz = e * f.bz;
 }
 
+// c ? a : b through PTX selp, opaque to the front end's array-index recovery
+__device__ __forceinline__ double select_f64(bool c, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %3, 0;\n\tselp.f64 %0, %1, %2, p;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"((int)c));
+  return r;
+}
+
 // compare-exchange on the integer pipe
 __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
   const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;

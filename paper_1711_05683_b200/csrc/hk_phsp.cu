@@ -155,7 +155,7 @@ template <int N>
 __device__ __forceinline__ double pick(const double (&p)[4 * N], int q, int c) {
   double v = 0.0;
 #pragma unroll
-  for (int j = 0; j < N; ++j) v = (j == q) ? p[4 * j + c] : v;
+  for (int j = 0; j < N; ++j) v = select_f64(j == q, p[4 * j + c], v);
   return v;
 }
 
@@ -179,7 +179,7 @@ __device__ __forceinline__ double pair_integrand(const double (&p)[4 * N],
 // phsp_generate -> phsp_average (phasespace.py:162-188 then :310-349) with the
 // event kept in registers: 0 bytes of HBM per event.
 template <int N, int MODE, bool PAIR>
-__global__ void __launch_bounds__(kBlock, PAIR ? GenMinBlocks<N>::value : 1)
+__global__ void __launch_bounds__(kBlock, PAIR ? GenShape<N>::min_blocks : 1)
     k_integrate(const __grid_constant__ IntArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
@@ -187,6 +187,33 @@ __global__ void __launch_bounds__(kBlock, PAIR ? GenMinBlocks<N>::value : 1)
                                   a.d.m_mother);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (PAIR && GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
+#pragma unroll 1
+      for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
+        const uint64_t row0 = a.ev_begin + (uint64_t)(c * HK_CHUNK + i * kBlock + threadIdx.x);
+        const uint64_t row1 = row0 + HK_CHUNK / 2;
+        double p0[4 * N], p1[4 * N];
+        const double w0 = rest_event<N, MODE>(a.d, a.rp, row0, p0);
+        const double w1 = rest_event<N, MODE>(a.d, a.rp, row1, p1);
+        const double f0 = pair_integrand<N>(p0, a.pair);
+        const double f1 = pair_integrand<N>(p1, a.pair);
+        if (!isfinite(f0)) record_bad(a.nonfinite_bad, row0);
+        if (!isfinite(f1)) record_bad(a.nonfinite_bad, row1);
+        const double ww0 = w0 * w0, ww1 = w1 * w1;
+        acc[0] += w0;
+        acc[1] += w0 * f0;
+        acc[2] += ww0;
+        acc[3] += ww0 * f0;
+        acc[4] += ww0 * f0 * f0;
+        acc[0] += w1;
+        acc[1] += w1 * f1;
+        acc[2] += ww1;
+        acc[3] += ww1 * f1;
+        acc[4] += ww1 * f1 * f1;
+      }
+      block_sum_store<5>(acc, a.part + 5 * c);
+      continue;
+    }
 #pragma unroll 1
     for (int i = 0; i < kRowsPerThread; ++i) {
       const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
@@ -330,62 +357,101 @@ struct GenChainArgs {
   unsigned long long* first_bad;
 };
 
+// Parent daughters other than the decaying one go to their spliced slots.
+// Compile-time recursion over J keeps p[] in registers (a runtime-trip loop
+// with a skip made nvcc demote p[] to local memory).
+template <int J, int N, int NS>
+__device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a,
+                                                       const double (&p)[4 * N], int64_t r) {
+  if constexpr (J < N) {
+    if (J != a.k) {
+      const int slot = 1 + 4 * (J < a.k ? J : J + NS - 1);
+      __stcs(a.cols[slot + 0] + r, p[4 * J + 0]);
+      __stcs(a.cols[slot + 1] + r, p[4 * J + 1]);
+      __stcs(a.cols[slot + 2] + r, p[4 * J + 2]);
+      __stcs(a.cols[slot + 3] + r, p[4 * J + 3]);
+    }
+    store_parent_daughters<J + 1, N, NS>(a, p, r);
+  }
+}
+
 // Fused phsp_generate + phsp_decay_chain (config C3): only the 4(n-1+n_sub)+1
 // final-state columns ever touch HBM.
+//
+// One fused chain event (generation, decay of daughter k, splice-ordered
+// stores); returns the event weight.  Branch-free apart from the moving-mother
+// test so two calls interleave; a mass mismatch lowers *bad to the row.
 template <int N, int NS, int MODE>
-__global__ void __launch_bounds__(kBlock) k_generate_chain(const __grid_constant__ GenChainArgs a) {
+__device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, int64_t r,
+                                            unsigned long long* bad) {
+  const uint64_t row = a.ev_begin + (uint64_t)r;
+  double p[4 * N];
+  const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
+  if (a.d.moving) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+  }
+  // daughter k's four-momentum; selp in asm so the front end cannot turn the
+  // select chain back into p[4k] (which demotes p[] to local memory)
+  double fe = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const bool sel = j == a.k;
+    fe = select_f64(sel, p[4 * j], fe);
+    fx = select_f64(sel, p[4 * j + 1], fx);
+    fy = select_f64(sel, p[4 * j + 2], fy);
+    fz = select_f64(sel, p[4 * j + 3], fz);
+  }
+  const double fm = frame_mass(fe, fx, fy, fz);
+  *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
+  double q[4 * NS];
+  const double ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
+  const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+  const double w = wp * ws;
+  __stcs(a.cols[0] + r, w);
+  store_parent_daughters<0, N, NS>(a, p, r);
+  const int sbase = 1 + 4 * a.k;
+#pragma unroll
+  for (int j = 0; j < 4 * NS; ++j) __stcs(a.cols[sbase + j] + r, q[j]);
+  return w;
+}
+
+template <int N, int NS, int MODE>
+__global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_constant__ GenChainArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
                                   a.d.m_mother);
+  unsigned long long bad = ~0ull;
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
+    if (N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
 #pragma unroll 1
-    for (int i = 0; i < kRowsPerThread; ++i) {
-      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
-      if (r < a.count) {
-        const uint64_t row = a.ev_begin + (uint64_t)r;
-        double p[4 * N];
-        const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
-        if (a.d.moving) {
-#pragma unroll
-          for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+      for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
+        const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
+        const double w0 = chain_row<N, NS, MODE>(a, mf, r0, &bad);
+        const double w1 = chain_row<N, NS, MODE>(a, mf, r0 + HK_CHUNK / 2, &bad);
+        acc[0] += w0;
+        acc[1] += w0 * w0;
+        acc[0] += w1;
+        acc[1] += w1 * w1;
+      }
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+        if (r < a.count) {
+          const double w = chain_row<N, NS, MODE>(a, mf, r, &bad);
+          acc[0] += w;
+          acc[1] += w * w;
         }
-        double fe = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          if (j == a.k) {
-            fe = p[4 * j];
-            fx = p[4 * j + 1];
-            fy = p[4 * j + 2];
-            fz = p[4 * j + 3];
-          }
-        }
-        const double fm = frame_mass(fe, fx, fy, fz);
-        if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
-        double q[4 * NS];
-        const double ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
-        const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
-        const double w = wp * ws;
-        __stcs(a.cols[0] + r, w);
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          if (j == a.k) continue;
-          const int slot = 1 + 4 * (j < a.k ? j : j + NS - 1);
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) __stcs(a.cols[slot + cc] + r, p[4 * j + cc]);
-        }
-        const int sbase = 1 + 4 * a.k;
-#pragma unroll
-        for (int j = 0; j < 4 * NS; ++j) __stcs(a.cols[sbase + j] + r, q[j]);
-        acc[0] += w;
-        acc[1] += w * w;
       }
     }
     if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
   }
+  if (bad != ~0ull) record_bad(a.first_bad, bad);
 }
 
 // ------------------------------------------------------------ unweighting --
