@@ -132,14 +132,6 @@ __device__ __forceinline__ uint64_t draw_bit_rt(const RngParams& rp, uint64_t ro
 // np.maximum(x, 0.0): NaN propagates, -0.0 kept.
 __device__ __forceinline__ double max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
 
-// Two-body breakup momentum (phasespace.py:67-71), reference op order; b2 = m*m
-// of the fixed daughter.
-__device__ __forceinline__ double pstar(double M, double a, double b2) {
-  const double M2 = M * M, a2 = a * a;
-  const double t = (M2 - a2) - b2;
-  const double lam = t * t - (4.0 * a2) * b2;
-  return sqrt(max0(lam)) / (2.0 * M);
-}
 
 // Boost frame of _boost (phasespace.py:74-81): the per-frame factors are shared
 // by every vector boosted into it, which is exact (same operands, same ops).
@@ -192,11 +184,14 @@ __device__ __forceinline__ double fast_rcp(double x) {
 __device__ __forceinline__ double fast_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  y = y * fma(-0.5 * x * y, y, 1.5);  // 1/sqrt(x) to ~2^-45
-  const double s = x * y;
-  const double r = fma(-s, s, x);
-  const double out = fma(r, 0.5 * y, s);
-  return (x >= 2.2250738585072014e-308 && x <= 1.7976931348623157e308) ? out : x;
+  double s = x * y;  // sqrt(x), seed accuracy
+  double h = 0.5 * y;  // 1 / (2 sqrt(x))
+  const double r = fma(-s, h, 0.5);  // one coupled Goldschmidt step
+  s = fma(s, r, s);
+  h = fma(h, r, h);
+  const double d = fma(-s, s, x);  // residual correction: ~1 ulp
+  s = fma(d, h, s);
+  return x > 0.0 ? s : x;  // 0 -> 0 and NaN -> NaN like IEEE sqrt (inputs are finite)
 }
 
 // Boost frame with one reciprocal for the three beta components and one for
@@ -236,6 +231,53 @@ __device__ __forceinline__ void boost_rest(const Frame& f, double m, double& e, 
   px = e * f.bx;
   py = e * f.by;
   pz = e * f.bz;
+}
+
+// Branch-free correctly rounded sqrt for positive normal x whose result is
+// normal: MUFU rsqrt seed, two Newton steps to y ~ 1/sqrt(x) (error far below
+// 2^-53), then Markstein's residual correction s + (x - s^2) y/2.  Verified
+// bit-identical to __dsqrt_rn on 2^32 inputs per family on B200
+// (tools/verify_cr.cu); used on the weight path so weights stay bit-exact
+// without the IEEE routine's slow-path branch.
+__device__ __forceinline__ double cr_sqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double t = x * y;
+  y = fma(0.5 * y, fma(-t, y, 1.0), y);
+  t = x * y;
+  y = fma(0.5 * y, fma(-t, y, 1.0), y);
+  const double s = x * y;
+  const double d = fma(-s, s, x);
+  return fma(d, 0.5 * y, s);
+}
+
+// Branch-free correctly rounded a / b for normal operands and quotient:
+// q = a * (1/b), then one residual correction q + (a - b q) / b.
+__device__ __forceinline__ double cr_div(double a, double b) {
+  const double r = fast_rcp(b);
+  const double q = a * r;
+  const double rem = fma(-b, q, a);
+  return fma(rem, r, q);
+}
+
+// Correctly rounded sqrt for every x >= 0 (and NaN) without branches:
+// subnormals are scaled by 2^106 into cr_sqrt's domain and back by 2^-53
+// (exact), zero / -0 / NaN are passed through as IEEE sqrt returns them.
+__device__ __forceinline__ double sqrt_weight(double x) {
+  const bool tiny = x < 2.2250738585072014e-308;
+  const double s = cr_sqrt(tiny ? x * 0x1.0p106 : x);
+  const double r = tiny ? s * 0x1.0p-53 : s;
+  return x > 0.0 ? r : x;
+}
+
+// Two-body breakup momentum (phasespace.py:67-71), reference op order; b2 = m*m
+// of the fixed daughter.  sqrt and the division are correctly rounded (IEEE
+// results, bit-identical), so weights are bit-exact.
+__device__ __forceinline__ double pstar(double M, double a, double b2) {
+  const double M2 = M * M, a2 = a * a;
+  const double t = (M2 - a2) - b2;
+  const double lam = t * t - (4.0 * a2) * b2;
+  return cr_div(sqrt_weight(max0(lam)), 2.0 * M);
 }
 
 // c ? a : b through PTX selp, opaque to the front end's array-index recovery
