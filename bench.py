@@ -54,6 +54,68 @@ def _traffic() -> float | None:
         return None
 
 
+class NvmlClockSampler:
+    """SM clock + clock-event reasons polled through NVML every ~2 ms in a
+    thread for exactly the timed region (the region is tens of ms, shorter
+    than nvidia-smi's sampling period).  Falls back to nvidia-smi."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.ok = False
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(visible.split(",")[self.gpu]) if visible else self.gpu
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi fallback
+            self.fallback = ClockSampler(self.gpu).__enter__()
+            return self
+        self.stop = threading.Event()
+
+        def poll():
+            nv, h = self.nv, self.h
+            while not self.stop.is_set():
+                try:
+                    self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                         nv.nvmlDeviceGetCurrentClocksEventReasons(h),
+                                         nv.nvmlDeviceGetPowerUsage(h) / 1000.0))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(0.002)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if not self.ok:
+            return self.fallback.__exit__(*exc)
+        self.stop.set()
+        self.thread.join(timeout=5)
+
+    def summary(self) -> dict:
+        if not self.ok:
+            return self.fallback.summary()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "source": "nvml"}
+        mhz = [s[0] for s in self.samples]
+        active = sorted({n for _, r, _ in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(mhz), "sm_min_mhz": min(mhz), "sm_max_mhz": self.max_mhz,
+                "power_w_max": max(s[2] for s in self.samples), "samples": len(self.samples),
+                "reasons": active, "source": "nvml, 2 ms polling inside the timed region"}
+
+
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -336,7 +398,7 @@ def run_ours(args) -> None:
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with NvmlClockSampler(local) as clocks:
         t0.record(st)
         for i in range(args.steps):
             tot = step(gen_ev[i])
