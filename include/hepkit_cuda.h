@@ -234,12 +234,20 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
 
-/* Yield-stationarity sums (fitting.py:401-434) for K <= 4 components: per
- * chunk K values sum_e r_k and K*K values sum_e r_k r_j, r_k = pdf_k(x)/density(x),
- * pdf_k = shape_k/norm_k.  Width K + K*K doubles per chunk.  density <= 0
- * (NaN included, fitting.py:418-420) -> *d_first_bad. */
+/* Yield-stationarity sums (fitting.py:401-434) and the sWeights matrix
+ * accumulation (splot.py:45-87) for K <= 4 components: per chunk K values
+ * sum_e r_k and K*K values sum_e r_k r_j, r_k = pdf_k(x)/density(x),
+ * pdf_k = shape_k/norm_k.  Width K + K*K doubles per chunk.
+ * d_first_bad[0]: first row with density not > 0 (NaN included,
+ * fitting.py:418-420); d_first_bad[1]: same or non-finite (splot.py:38). */
 int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                       uint64_t* d_first_bad, void* stream);
+
+/* sWeights table (splot.py:90-117): d_out[s][i] = sum_j V[s*K+j] pdf_j(x_i) / density(x_i)
+ * for K <= 4 species; V is a host K*K row-major matrix.  Non-positive or
+ * non-finite density -> *d_first_bad. */
+int hk_splot_weights(const double* d_x, int64_t n, const hk_model_t* model, const double* V,
+                     double* const* d_out, uint64_t* d_first_bad, void* stream);
 
 /* density(x) for n values (the value the error message quotes). */
 int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,

@@ -38,7 +38,7 @@ EXPORTS = (
     "hk_phsp_generate", "hk_phsp_generate_host", "hk_phsp_decay_chain", "hk_phsp_generate_chain",
     "hk_phsp_moments", "hk_map_program", "hk_phsp_integrate", "hk_fold_partials",
     "hk_nll_partials", "hk_nll_eval", "hk_model_density",
-    "hk_yield_partials",
+    "hk_yield_partials", "hk_splot_weights",
     "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
 )
 
@@ -119,6 +119,7 @@ _SIGS = {
     "hk_nll_eval": (_INT, [_P, _I64, _M, _P, _PD, _PU, _P]),
     "hk_model_density": (_INT, [_P, _I64, _M, _P, _P]),
     "hk_yield_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
+    "hk_splot_weights": (_INT, [_P, _I64, _M, _PD, _PP, _P, _P]),
     "hk_unweight_flags": (_INT, [_P, _I64, ctypes.c_double, _K, _U64, _P, _P, _P, _P]),
     "hk_compact": (_INT, [_PP, _I32, _I64, _P, _P, _PP, _I32, _P]),
     "hk_scan_counts": (_INT, [_P, _I64, _P, _P, _P]),

@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(kBlock) k_yield(const double* __restrict__ x, 
         }
         d += p[k] * c.yield[k];
       }
+      // [0]: density not > 0 (fitting.py:418); [1]: also non-finite (splot.py:38)
       if (!(d > 0.0)) record_bad(first_bad, (uint64_t)r);
+      if (first_bad && (!(d > 0.0) || !isfinite(d))) record_bad(first_bad + 1, (uint64_t)r);
       const double inv = 1.0 / d;
 #pragma unroll
       for (int k = 0; k < K; ++k) p[k] *= inv;
@@ -283,6 +285,71 @@ int launch_nll(const double* d_x, int64_t n, const Coeffs& c, double* part,
   else
     k_nll<false><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad);
   return check_launch("k_nll");
+}
+
+// pdf_k coefficients (no yields in amp) for the yield / sPlot kernels
+int make_pdf_coeffs(const hk_model_t* model, PdfCoeffs* c) {
+  std::memset(c, 0, sizeof(*c));
+  const double sqrt2pi = 2.5066282746310002;
+  for (int k = 0; k < model->n_comp; ++k) {
+    c->kind[k] = model->kind[k];
+    c->yield[k] = model->yield[k];
+    if (model->kind[k] == HK_SHAPE_GAUSS) {
+      HK_REQUIRE(model->p1[k] > 0, "component %d: sigma must be positive", k);
+      c->amp[k] = 1.0 / (model->p1[k] * sqrt2pi * model->norm[k]);
+      c->shift[k] = model->p0[k];
+      c->scale[k] = 1.0 / model->p1[k];
+    } else if (model->kind[k] == HK_SHAPE_EXPO) {
+      HK_REQUIRE(model->p0[k] != 0, "component %d: tau must be non-zero", k);
+      c->amp[k] = 1.0 / model->norm[k];
+      c->scale[k] = -1.0 / model->p0[k];
+    } else {
+      set_error("component %d: unknown shape kind %d", k, model->kind[k]);
+      return HK_EUNSUPPORTED;
+    }
+  }
+  return HK_OK;
+}
+
+// sWeights (splot.py:90-117): sw_n(e) = sum_j V_nj pdf_j(x_e) / density(x_e)
+struct SplotArgs {
+  PdfCoeffs c;
+  int32_t k;
+  double V[16];
+  double* out[4];
+  unsigned long long* bad;  // density <= 0 or non-finite (splot.py:35-42)
+};
+
+__global__ void __launch_bounds__(kBlock) k_splot(const double* __restrict__ x, int64_t n,
+                                                  const __grid_constant__ SplotArgs a) {
+  const int64_t r = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (r >= n) return;
+  const double xv = __ldg(x + r);
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  double d = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < a.k) {
+      if (a.c.kind[k] == HK_SHAPE_GAUSS) {
+        const double z = (xv - a.c.shift[k]) * a.c.scale[k];
+        p[k] = a.c.amp[k] * exp(-0.5 * z * z);
+      } else {
+        p[k] = a.c.amp[k] * exp(xv * a.c.scale[k]);
+      }
+      d += p[k] * a.c.yield[k];
+    }
+  }
+  if (!(d > 0.0) || !isfinite(d)) record_bad(a.bad, (uint64_t)r);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (s < a.k) {
+      double num = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < a.k) num += p[j] * a.V[s * a.k + j];
+      a.out[s][r] = num / d;
+    }
+  }
 }
 
 // Mapped pinned mailbox per (host thread, device) for hk_nll_eval:
@@ -382,25 +449,7 @@ int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, dou
   HK_REQUIRE(model && model->n_comp >= 1 && model->n_comp <= 4,
              "yield stationarity supports 1..4 components");
   PdfCoeffs c;
-  std::memset(&c, 0, sizeof(c));
-  const double sqrt2pi = 2.5066282746310002;
-  for (int k = 0; k < model->n_comp; ++k) {
-    c.kind[k] = model->kind[k];
-    c.yield[k] = model->yield[k];
-    if (model->kind[k] == HK_SHAPE_GAUSS) {
-      HK_REQUIRE(model->p1[k] > 0, "component %d: sigma must be positive", k);
-      c.amp[k] = 1.0 / (model->p1[k] * sqrt2pi * model->norm[k]);
-      c.shift[k] = model->p0[k];
-      c.scale[k] = 1.0 / model->p1[k];
-    } else if (model->kind[k] == HK_SHAPE_EXPO) {
-      HK_REQUIRE(model->p0[k] != 0, "component %d: tau must be non-zero", k);
-      c.amp[k] = 1.0 / model->norm[k];
-      c.scale[k] = -1.0 / model->p0[k];
-    } else {
-      set_error("component %d: unknown shape kind %d", k, model->kind[k]);
-      return HK_EUNSUPPORTED;
-    }
-  }
+  if (int rc = make_pdf_coeffs(model, &c)) return rc;
   HK_REQUIRE(n >= 0, "negative n");
   if (n == 0) return HK_OK;
   HK_REQUIRE(d_x && d_partials, "NULL pointer");
@@ -414,6 +463,27 @@ int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, dou
     default: k_yield<4><<<grid, kBlock, 0, st>>>(d_x, n, c, d_partials, bad); break;
   }
   return check_launch("k_yield");
+}
+
+int hk_splot_weights(const double* d_x, int64_t n, const hk_model_t* model, const double* V,
+                     double* const* d_out, uint64_t* d_first_bad, void* stream) {
+  HK_REQUIRE(model && model->n_comp >= 1 && model->n_comp <= 4, "sPlot supports 1..4 species");
+  HK_REQUIRE(V && d_out, "NULL pointer");
+  SplotArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (int rc = make_pdf_coeffs(model, &a.c)) return rc;
+  a.k = model->n_comp;
+  for (int i = 0; i < a.k * a.k; ++i) a.V[i] = V[i];
+  for (int i = 0; i < a.k; ++i) {
+    HK_REQUIRE(d_out[i], "output column %d NULL", i);
+    a.out[i] = d_out[i];
+  }
+  a.bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_x, "NULL data");
+  k_splot<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, as_stream(stream)>>>(d_x, n, a);
+  return check_launch("k_splot");
 }
 
 int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,
