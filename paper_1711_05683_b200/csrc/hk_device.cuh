@@ -260,14 +260,13 @@ __device__ __forceinline__ double cr_div(double a, double b) {
   return fma(rem, r, q);
 }
 
-// Correctly rounded sqrt for every x >= 0 (and NaN) without branches:
-// subnormals are scaled by 2^106 into cr_sqrt's domain and back by 2^-53
-// (exact), zero / -0 / NaN are passed through as IEEE sqrt returns them.
-__device__ __forceinline__ double sqrt_weight(double x) {
-  const bool tiny = x < 2.2250738585072014e-308;
-  const double s = cr_sqrt(tiny ? x * 0x1.0p106 : x);
-  const double r = tiny ? s * 0x1.0p-53 : s;
-  return x > 0.0 ? r : x;
+// sqrt(np.maximum(lam, 0)) for the Kallen lambda: correctly rounded for
+// lam > 0, 0 for lam <= 0, NaN propagated.  lam = t*t - (4 a2) b2 of GeV-scale
+// squares is either 0 or >= ~1e-20 (a multiple of ulp(t*t)), never subnormal,
+// so cr_sqrt's normal-range domain covers it.
+__device__ __forceinline__ double sqrt_lambda(double lam) {
+  const double s = cr_sqrt(lam);
+  return lam > 0.0 ? s : (lam == lam ? 0.0 : lam);
 }
 
 // Two-body breakup momentum (phasespace.py:67-71), reference op order; b2 = m*m
@@ -277,7 +276,7 @@ __device__ __forceinline__ double pstar(double M, double a, double b2) {
   const double M2 = M * M, a2 = a * a;
   const double t = (M2 - a2) - b2;
   const double lam = t * t - (4.0 * a2) * b2;
-  return cr_div(sqrt_weight(max0(lam)), 2.0 * M);
+  return cr_div(sqrt_lambda(lam), 2.0 * M);
 }
 
 // c ? a : b through PTX selp, opaque to the front end's array-index recovery
@@ -332,7 +331,9 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
     // phi = 2 pi u: sincospi(2u) needs no Payne-Hanek reduction and differs
     // from cos(fl(2 pi u)) by at most the rounding of fl(2 pi u) (<= 4.4e-16)
     const double two_u = 2.0 * to_unit(bits[N - 2 + 2 * (k - 1) + 1]);
-    const double sz = fast_sqrt(max0(1.0 - cz * cz));  // cancellation-sensitive: no FMA
+    // 1 - cz^2 >= 0 exactly (|cz| <= 1), so np.maximum is a no-op here;
+    // cancellation-sensitive: no FMA
+    const double sz = fast_sqrt(1.0 - cz * cz);
     double sn, cs;
     math::k_sincospi(two_u, &sn, &cs);
     const double nx = sz * cs, ny = sz * sn, nz = cz;
