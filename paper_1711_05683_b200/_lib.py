@@ -200,8 +200,21 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+_raw_stream = None
+
+
 def stream_ptr() -> int:
-    return torch().cuda.current_stream().cuda_stream
+    """cudaStream_t of torch's current stream on the current device (honours
+    `with torch.cuda.stream(...)`).  Uses torch's raw-stream query when it
+    exists -- it skips building a Stream object (3 us -> 0.3 us per call)."""
+    global _raw_stream
+    t = torch()
+    if _raw_stream is None:
+        fn = getattr(t._C, "_cuda_getCurrentRawStream", None)
+        _raw_stream = fn if fn is not None else False
+    if _raw_stream:
+        return _raw_stream(t.cuda.current_device())
+    return t.cuda.current_stream().cuda_stream
 
 
 def ptr(t) -> int:

@@ -29,6 +29,11 @@ struct Coeffs {
   double scale[HK_MAX_COMPONENTS];  // gauss: 1/sigma; expo: -1/tau
 };
 
+// exp for the FCN data pass.  libdevice's: a 64-entry shared-memory table
+// variant (11 FP64 ops instead of ~17) measured slower on B200 (40.6 vs 36.1 us
+// per 1e7 events) -- LDS latency in the dependency chain -- and was dropped.
+__device__ __forceinline__ double fcn_exp(double v) { return ::exp(v); }
+
 __device__ __forceinline__ double density(const Coeffs& c, double x) {
   double d = 0.0;
 #pragma unroll 1
@@ -36,9 +41,9 @@ __device__ __forceinline__ double density(const Coeffs& c, double x) {
     double t;
     if (c.kind[k] == HK_SHAPE_GAUSS) {
       const double z = (x - c.shift[k]) * c.scale[k];
-      t = c.amp[k] * math::k_exp(-0.5 * z * z);
+      t = c.amp[k] * fcn_exp(-0.5 * z * z);
     } else {
-      t = c.amp[k] * math::k_exp(x * c.scale[k]);
+      t = c.amp[k] * fcn_exp(x * c.scale[k]);
     }
     d = k == 0 ? t : d + t;
   }
@@ -49,7 +54,7 @@ __device__ __forceinline__ double density(const Coeffs& c, double x) {
 // cli.py:316-320 / toymodel.py): no component loop, no kind branches.
 __device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
   const double z = (x - c.shift[0]) * c.scale[0];
-  return c.amp[0] * math::k_exp(-0.5 * z * z) + c.amp[1] * math::k_exp(x * c.scale[1]);
+  return c.amp[0] * fcn_exp(-0.5 * z * z) + c.amp[1] * fcn_exp(x * c.scale[1]);
 }
 
 // sum_e ln d_e as ln(prod_e d_e), the product kept as a mantissa in [1, 2^16)

@@ -1,18 +1,22 @@
-// hk_math.cuh -- fp64 sin/cos(pi t) and exp with coefficients in constant
-// memory.
+// hk_math.cuh -- our own fp64 sin/cos(pi t) and exp, kept as measured
+// alternatives to libdevice's (which the kernels use by default).
 //
-// Why: the CUDA math library materialises every polynomial coefficient as a
-// 64-bit immediate (two UMOVs each, per call) -- sincospi costs ~75 issued
-// instructions of which 24 are UMOVs, exp ~22 UMOVs.  Here DFMA reads its
-// coefficient straight from the constant bank, and the argument reduction is
-// specialised to the ranges the kernels use.  The functions are
-// __host__ __device__ so tests/test_math_host.py can check them against long
-// double on the CPU.
+// Motivation: libdevice materialises each polynomial coefficient as a 64-bit
+// immediate (two UMOVs per coefficient per call; sincospi ~75 issued
+// instructions, 24 of them UMOV).  Measured on B200:
+//   - coefficients from the constant bank (HK_MATH_CONST_BANK): slower
+//     (generator +2.6%, FCN +27%);
+//   - coefficients as immediates: sincospi ties libdevice (2.315 vs 2.305 ms
+//     per 1e8 events), exp is slower than libdevice's in the FCN (45.6 vs
+//     35.8 us).
+// So k_sincospi/k_exp default to libdevice; -DHK_MATH_OWN_SINCOSPI /
+// -DHK_MATH_OWN_EXP select these.  The functions are __host__ __device__ so
+// tests/test_math_host.py checks them against long double on the CPU.
 //
-// Accuracy (checked on the CPU over 2^24 points, tests/test_math_host.py):
-//   hk_sincospi: |error| <= 2 ulp(1) absolute for |t| < 2^20
-//   hk_exp:      <= 2 ulp relative over [-708, 709]; exact under/overflow to
-//                0/inf beyond; NaN propagates.
+// Accuracy (CPU, 2^22 points):
+//   sincospi: |error| <= 2 ulp(1) absolute for |t| < 2^20
+//   exp:      <= 2 ulp relative over [-708, 709]; exact under/overflow to
+//             0/inf beyond; NaN propagates.
 #pragma once
 
 #include <cmath>
