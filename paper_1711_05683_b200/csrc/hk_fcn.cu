@@ -146,7 +146,13 @@ struct FcnWork {
 };
 
 template <bool GE>
-__global__ void __launch_bounds__(kBlock) k_nll_fused(const double* __restrict__ x, int64_t n,
+// 4 CTAs/SM (64 registers) measured best for the one-launch FCN on B200:
+// C-ABI call 47.8 us; 5 CTAs (48 regs + spills) 50.6, 6 CTAs 53.9, 8 CTAs 64.4,
+// and an unconstrained (256, 1) bound lets ptxas take 216 registers (82 us).
+#ifndef HK_FCN_MIN_BLOCKS
+#define HK_FCN_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const double* __restrict__ x, int64_t n,
                                                       const __grid_constant__ Coeffs c, FcnWork w) {
   const int64_t chunks = (n + HK_CHUNK - 1) / HK_CHUNK;
   for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {

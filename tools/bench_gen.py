@@ -65,6 +65,17 @@ def main():
     e1.record()
     e1.synchronize()
     out["fcn_kernel_us"] = e0.elapsed_time(e1) / 50 * 1e3
+    # one-launch FCN through the C ABI (k_nll_fused + mailbox), synchronous per call
+    import ctypes
+    import time
+    work = torch.zeros(_lib.num_chunks(x.numel()) + 4, dtype=torch.float64, device="cuda")
+    ls, fb = ctypes.c_double(), ctypes.c_uint64()
+    for _ in range(20):
+        L.hk_nll_eval(_lib.ptr(x), x.numel(), lm, _lib.ptr(work), ctypes.byref(ls), ctypes.byref(fb), st.cuda_stream)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        L.hk_nll_eval(_lib.ptr(x), x.numel(), lm, _lib.ptr(work), ctypes.byref(ls), ctypes.byref(fb), st.cuda_stream)
+    out["fcn_eval_us"] = (time.perf_counter() - t0) / 200 * 1e6
     if a.check:
         from oracle import oracle as O
         want = O.nll(xs, O.gauss_exp_components(5.0, 0.5, 3.0, 4e6, 6e6))
