@@ -239,7 +239,7 @@ def fcn_bench(hk, torch, evals: int = 200) -> dict:
     from paper_1711_05683_b200.fitting import lower_model
     x = data.device_column("x0")
     lm = lower_model(model)
-    parts = _lib.empty(_lib.num_chunks(FCN_EVENTS))
+    parts = _lib.empty(_lib.num_fcn_tiles(FCN_EVENTS))
     bad = _lib.bad_cells(1)
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -252,7 +252,7 @@ def fcn_bench(hk, torch, evals: int = 200) -> dict:
     ev1.synchronize()
     kt = ev0.elapsed_time(ev1) / evals * 1e-3
     # the one-launch C-ABI FCN call alone (kernel + 16-byte readback + sync), no Python model lowering
-    work = torch.zeros(_lib.num_chunks(FCN_EVENTS) + 4, dtype=torch.float64, device=x.device)
+    work = torch.zeros(_lib.num_fcn_tiles(FCN_EVENTS) + 4, dtype=torch.float64, device=x.device)
     logsum, first = ctypes.c_double(), ctypes.c_uint64()
     for _ in range(3):
         _lib.lib().hk_nll_eval(_lib.ptr(x), FCN_EVENTS, lm, _lib.ptr(work), ctypes.byref(logsum),

@@ -220,17 +220,21 @@ int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, d
                      void* stream);
 
 /* ------------------------------------------------------------------- FCN */
-/* Extended NLL event sum (fitting.py:197-207): per chunk sum_e ln density(x_e);
+/* The FCN reduces per HK_FCN_TILE rows (a divisor of HK_CHUNK, so chunk-
+ * aligned shards stay tile-aligned): ceil(n / HK_FCN_TILE) partials. */
+#define HK_FCN_TILE 4096
+
+/* Extended NLL event sum (fitting.py:197-207): per tile sum_e ln density(x_e);
  * density <= 0 or non-finite -> *d_first_bad (fitting.py:200-205). */
 int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                     uint64_t* d_first_bad, void* stream);
 
-/* One FCN evaluation end to end: partials + fold + 16-byte readback.
- * Synchronous.  *h_logsum = sum_e ln density; *h_first_bad = first failing
- * row or HK_NO_BAD_ROW.  One kernel launch (the last CTA folds the chunk
- * partials in a fixed order) plus one 16-byte readback.  d_work needs
- * hk_num_chunks(n) + 4 doubles, ZERO-FILLED before its first use; the kernel
- * re-arms it for the next call. */
+/* One FCN evaluation end to end.  Synchronous.  *h_logsum = sum_e ln density;
+ * *h_first_bad = first failing row or HK_NO_BAD_ROW.  One kernel launch (the
+ * last CTA folds the tile partials in a fixed order and publishes the result
+ * into mapped pinned host memory, which the caller's thread polls).  d_work
+ * needs ceil(n / HK_FCN_TILE) + 4 doubles, ZERO-FILLED before its first use;
+ * the kernel re-arms it for the next call. */
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
 

@@ -278,6 +278,13 @@ def num_chunks(n: int) -> int:
     return (int(n) + HK_CHUNK - 1) // HK_CHUNK
 
 
+HK_FCN_TILE = 4096   # rows per FCN partial (include/hepkit_cuda.h)
+
+
+def num_fcn_tiles(n: int) -> int:
+    return (int(n) + HK_FCN_TILE - 1) // HK_FCN_TILE
+
+
 def fold(partials, n_parts: int, width: int):
     """Deterministic device fold of (n_parts, width) partials -> (width,) tensor."""
     out = empty(width)

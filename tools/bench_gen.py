@@ -55,7 +55,7 @@ def main():
     model = hk.add_pdfs([hk.Parameter("n_sig", 4e6), hk.Parameter("n_bkg", 6e6)],
                         [hk.make_pdf(g, hk.gaussian_norm(g), reg), hk.make_pdf(e, hk.exponential_norm(e), reg)])
     lm = lower_model(model)
-    parts = _lib.empty(_lib.num_chunks(x.numel()))
+    parts = _lib.empty(_lib.num_fcn_tiles(x.numel()))
     bad = _lib.bad_cells(1)
     for _ in range(3):
         L.hk_nll_partials(_lib.ptr(x), x.numel(), lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
@@ -68,7 +68,7 @@ def main():
     # one-launch FCN through the C ABI (k_nll_fused + mailbox), synchronous per call
     import ctypes
     import time
-    work = torch.zeros(_lib.num_chunks(x.numel()) + 4, dtype=torch.float64, device="cuda")
+    work = torch.zeros(_lib.num_fcn_tiles(x.numel()) + 4, dtype=torch.float64, device="cuda")
     ls, fb = ctypes.c_double(), ctypes.c_uint64()
     for _ in range(20):
         L.hk_nll_eval(_lib.ptr(x), x.numel(), lm, _lib.ptr(work), ctypes.byref(ls), ctypes.byref(fb), st.cuda_stream)
