@@ -43,9 +43,26 @@ __host__ __device__ __forceinline__ uint64_t key_base(uint64_t seed, uint64_t st
   return mix64(seed + kGolden) ^ mix64(stream * kSalt + kGolden);
 }
 
+// x * 2^-s for a non-negative integer-valued double x < 2^53, on the integer
+// pipe: subtract s from the exponent field (exact; x = 0 stays 0).  Keeps the
+// FP64 pipe -- the generator's binding resource -- free of the scaling DMULs.
+__device__ __forceinline__ double scale_down(double x, int s) {
+  const long long b = __double_as_longlong(x);
+  return b == 0 ? 0.0 : __longlong_as_double(b - ((long long)s << 52));
+}
+
 // top 53 bits -> [0, 1), exact (rng.py:125)
 __device__ __forceinline__ double to_unit(uint64_t bits53) {
-  return __ull2double_rn(bits53) * kInv53;
+  return scale_down(__ull2double_rn(bits53), 53);
+}
+
+// 2u and 2u - 1 for u = bits53 * 2^-53: both exact in the first step, so the
+// single rounding of the fma equals numpy's 2.0 * u - 1.0 (phasespace.py:135-136)
+__device__ __forceinline__ double two_unit(uint64_t bits53) {
+  return scale_down(__ull2double_rn(bits53), 52);
+}
+__device__ __forceinline__ double two_unit_minus_one(uint64_t bits53) {
+  return fma(__ull2double_rn(bits53), 0x1.0p-52, -1.0);
 }
 
 // Philox4x32-10 (Salmon et al., SC'11); counter = (row lo, row hi, block, tag).
@@ -327,10 +344,10 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
 #pragma unroll
   for (int k = 1; k < N; ++k) {
     const double q = ps[k];
-    const double cz = 2.0 * to_unit(bits[N - 2 + 2 * (k - 1)]) - 1.0;
+    const double cz = two_unit_minus_one(bits[N - 2 + 2 * (k - 1)]);
     // phi = 2 pi u: sincospi(2u) needs no Payne-Hanek reduction and differs
     // from cos(fl(2 pi u)) by at most the rounding of fl(2 pi u) (<= 4.4e-16)
-    const double two_u = 2.0 * to_unit(bits[N - 2 + 2 * (k - 1) + 1]);
+    const double two_u = two_unit(bits[N - 2 + 2 * (k - 1) + 1]);
     // 1 - cz^2 >= 0 exactly (|cz| <= 1), so np.maximum is a no-op here;
     // cancellation-sensitive: no FMA
     const double sz = fast_sqrt(1.0 - cz * cz);
