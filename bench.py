@@ -377,7 +377,7 @@ def run_ours(args) -> None:
     k = _lib.make_key(key)
     cols = [_lib.empty(n) for _ in range(13)]
     colp = _lib.ptr_array(cols)
-    wpart = _lib.empty(2 * _lib.num_chunks(n))
+    wpart = _lib.empty(2 * _lib.num_weight_slices(n))
     st = torch.cuda.current_stream()
     L = _lib.lib()
 
@@ -387,8 +387,8 @@ def run_ours(args) -> None:
         _lib.check(L.hk_phsp_generate(d, k, rank * n, n, colp, _lib.ptr(wpart), st.cuda_stream), "generate")
         if gen_events:
             gen_events[1].record(st)
-        full = gather_partials(wpart, n_total, 2)
-        return _lib.fold(full, _lib.num_chunks(n_total), 2)
+        full = gather_partials(wpart, n_total, 2 * _lib.HK_WARP_SLICES)   # per chunk: 8 slices x 2
+        return _lib.fold(full, _lib.num_weight_slices(n_total), 2)
 
     for _ in range(args.warmup):
         tot = step()

@@ -42,6 +42,7 @@ extern "C" {
 #define HK_EUNSUPPORTED 4 /* configuration outside the compiled kernels */
 
 #define HK_CHUNK 4096        /* rows per reduction partial (parallel.py:18) */
+#define HK_WARP_SLICES 8     /* per-warp weight partials per chunk (generation kernels) */
 #define HK_MAX_DAUGHTERS 16  /* templated fast path covers n <= 8 */
 #define HK_MAX_PROGRAM 48    /* ops per device functor program */
 #define HK_MAX_SLOTS 16      /* virtual registers per program */
@@ -145,8 +146,10 @@ int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, d
 /* phsp_generate (phasespace.py:162-188) for rows [ev_begin, ev_begin+ev_count):
  * writes 4n+1 columns, d_cols[0] = weight, d_cols[1+4j+c] = daughter j+1,
  * component c (e, px, py, pz) (phsp_schema, phasespace.py:60-64).
- * d_wpartials (optional, NULL to skip): 2 doubles per chunk = (sum w, sum w^2),
- * the weight-integration moments fused into the same pass. */
+ * d_wpartials (optional, NULL to skip): (sum w, sum w^2) per warp-slice --
+ * HK_WARP_SLICES slices per 4096-row chunk, 2 * HK_WARP_SLICES * chunks
+ * doubles -- the weight-integration moments fused into the same pass without
+ * a CTA barrier; fold them with hk_fold_partials(n_parts = slices, width 2). */
 int hk_phsp_generate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
                      int64_t ev_count, double* const* d_cols, double* d_wpartials, void* stream);
 

@@ -279,6 +279,12 @@ def num_chunks(n: int) -> int:
 
 
 HK_FCN_TILE = 4096   # rows per FCN partial (include/hepkit_cuda.h)
+HK_WARP_SLICES = 8   # per-warp weight partials per chunk (generation kernels)
+
+
+def num_weight_slices(n: int) -> int:
+    """Number of (sum w, sum w^2) partials the generation kernels write for n rows."""
+    return HK_WARP_SLICES * num_chunks(n)
 
 
 def num_fcn_tiles(n: int) -> int:

@@ -445,6 +445,24 @@ __device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
   __syncthreads();
 }
 
+// Per-warp partials (no CTA barrier): a fixed shuffle tree inside the warp,
+// lane 0 stores W doubles for warp-slice (chunk, warp) at
+// out[W * (chunk * HK_WARP_SLICES + warp) ..].  The host folds the slices in
+// index order, so the result is as deterministic as a CTA reduction.
+template <int W>
+__device__ __forceinline__ void warp_sum_store(double (&v)[W], double* out, int64_t chunk) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] += __shfl_down_sync(0xffffffffu, v[w], off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    double* dst = out + (int64_t)W * (chunk * HK_WARP_SLICES + (threadIdx.x >> 5));
+#pragma unroll
+    for (int w = 0; w < W; ++w) dst[w] = v[w];
+  }
+}
+
 __device__ __forceinline__ void record_bad(unsigned long long* first_bad, uint64_t row) {
   if (first_bad) atomicMin(first_bad, (unsigned long long)row);
 }

@@ -46,7 +46,7 @@ struct GenArgs {
   uint64_t ev_begin;
   int64_t count;
   double* cols[kMaxCols];  // all NULL = no store
-  double* wpart;           // 2 doubles per chunk or NULL
+  double* wpart;           // 2 doubles per warp-slice (HK_WARP_SLICES per chunk) or NULL
   int store;
 };
 
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         acc[0] += w1;
         acc[1] += w1 * w1;
       }
-      if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+      if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
       continue;
     }
 #pragma unroll 1
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         acc[1] += w * w;
       }
     }
-    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
   }
 }
 
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kBlock) k_generate_rt(const __grid_constant__ 
         acc[1] += w * w;
       }
     }
-    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
   }
 }
 
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_const
         }
       }
     }
-    if (a.wpart) block_sum_store<2>(acc, a.wpart + 2 * c);
+    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
   }
   if (bad != ~0ull) record_bad(a.first_bad, bad);
 }

@@ -101,8 +101,7 @@ def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKe
     store = ColumnStore._from_device(phsp_schema(spec.n), cols)
     if n_events == 0:
         return store
-    nch = _lib.num_chunks(n_events)
-    wpart = _lib.empty(2 * nch)
+    wpart = _lib.empty(2 * _lib.num_weight_slices(n_events))
     _lib.check(_lib.lib().hk_phsp_generate(d, k, _lib.u64(row_offset), n_events, _lib.ptr_array(cols),
                                            _lib.ptr(wpart), _lib.stream_ptr()), "hk_phsp_generate")
     store.meta["weight_partials"] = wpart
@@ -125,7 +124,7 @@ def phsp_generate_to_host(spec: DecaySpec, mother: FourVector, n_events: int, ke
     ncols = 4 * spec.n + 1
     if out is None:
         out = [torch.empty(n_events, dtype=torch.float64, pin_memory=True) for _ in range(ncols)]
-    head = (2 * _lib.num_chunks(n_events) + 2) * 8
+    head = (2 * _lib.num_weight_slices(n_events) + 2) * 8
     stage_bytes = max(int(stage_bytes), head + 2 * ncols * 8 * _lib.HK_CHUNK)
     stage = _stage_buffer(stage_bytes)
     sums = (ctypes.c_double * 2)()
@@ -193,7 +192,7 @@ def phsp_weight_moments(block: ColumnStore) -> WeightMoments:
         parts5 = _moment_partials(block, prog)
         tot = _lib.fold(parts5, _lib.num_chunks(n), 5).cpu().numpy()
         return WeightMoments(n, float(tot[0]), float(tot[2]))
-    tot = _lib.fold(parts, _lib.num_chunks(n), 2).cpu().numpy()
+    tot = _lib.fold(parts, _lib.num_weight_slices(n), 2).cpu().numpy()
     return WeightMoments(n, float(tot[0]), float(tot[1]))
 
 
@@ -363,7 +362,7 @@ def phsp_generate_chain(spec: DecaySpec, mother: FourVector, n_events: int, key:
     if n_events == 0:
         return store
     mode = rng_mode(rng)
-    wpart = _lib.empty(2 * _lib.num_chunks(n_events))
+    wpart = _lib.empty(2 * _lib.num_weight_slices(n_events))
     bad = _lib.bad_cells(1)
     _lib.check(_lib.lib().hk_phsp_generate_chain(
         _lib.make_decay(spec, mother, m_mother), _lib.make_key(key, mode), int(daughter_index),

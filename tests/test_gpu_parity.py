@@ -417,7 +417,7 @@ def test_sharded_runs_bitwise_invariant(cuda, hk):
     spec, mother = _b0(hk)
     n = 2_000_003
     one = hk.phsp_generate(spec, mother, n, hk.RngKey(1, 1))
-    ref_tot = _lib.fold(one.meta["weight_partials"], _lib.num_chunks(n), 2).cpu().numpy()
+    ref_tot = _lib.fold(one.meta["weight_partials"], _lib.num_weight_slices(n), 2).cpu().numpy()
     for world in (2, 4, 8):
         parts, cols = [], []
         for r in range(world):
@@ -426,5 +426,5 @@ def test_sharded_runs_bitwise_invariant(cuda, hk):
             parts.append(s.meta["weight_partials"])
             cols.append(s.device_column("p2_px"))
         assert torch.equal(torch.cat(cols), one.device_column("p2_px"))
-        tot = _lib.fold(torch.cat(parts), _lib.num_chunks(n), 2).cpu().numpy()
+        tot = _lib.fold(torch.cat(parts), _lib.num_weight_slices(n), 2).cpu().numpy()
         assert np.array_equal(tot, ref_tot), world

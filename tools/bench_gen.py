@@ -30,7 +30,7 @@ def main():
     k = _lib.make_key(hk.RngKey(1, 1), hk.rng.rng_mode(a.rng))
     cols = [_lib.empty(n) for _ in range(13)]
     cp = _lib.ptr_array(cols)
-    wp = _lib.empty(2 * _lib.num_chunks(n))
+    wp = _lib.empty(2 * _lib.num_weight_slices(n))
     st = torch.cuda.current_stream()
     L = _lib.lib()
     for _ in range(3):
