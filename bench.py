@@ -334,6 +334,23 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         pz = cols["p1_pz"] + cols["p2_pz"]
         return (e * e - px * px - py * py - pz * pz,)
 
+    # C2-average: phsp_average(<m12^2>) over a stored 1e8 block (interpreter over HBM columns:
+    # reads p1, p2 four-momenta + weight = 72 B/event)
+    blk = hk.phsp_generate(spec, mother, EVENTS_PER_GPU, hk.RngKey(1, 1), row_offset=rank * EVENTS_PER_GPU)
+    res = {}
+
+    def c2avg():
+        res["r"] = hk.phsp_average(hk.identity(), blk, m12)
+
+    dt = _timed(torch, c2avg, 10, dist)
+    out["C2_average"] = {"workload": "phsp_average(<m12^2>) over a stored 1e8-event block per GPU "
+                                     "(public API, 72 B/event read)",
+                         "value": world * EVENTS_PER_GPU / dt, "unit": "events/s", "ms_per_call": dt * 1e3,
+                         "hbm_GBps_per_gpu": 72 * EVENTS_PER_GPU / dt / 1e9,
+                         "frac_of_measured_copy_bw": 72 * EVENTS_PER_GPU / dt / 1e9 / peak,
+                         "m12sq_average": float(res["r"].value)}
+    del blk
+    torch.cuda.empty_cache()
     n5 = 10_000_000_000
     a, b = shard_range(n5, rank, world)
     res = {}

@@ -194,6 +194,26 @@ int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_coun
 int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const hk_program_t* f,
                    double* d_out, uint64_t* d_first_bad, void* stream);
 
+/* Runtime specialisation of functor programs, the GPU analogue of Hydra's
+ * compile-time functor instantiation: hk_phsp_moments / hk_map_program emit
+ * the program as straight-line CUDA, compile it with NVRTC for sm_100a
+ * (no FMA contraction, same rounding as the interpreter: results are
+ * bit-identical) and cache the cubin per program.  mode 0 = always interpret,
+ * 1 = always specialise (HK_ECUDA if NVRTC is unavailable), 2 = auto
+ * (specialise when >= HK_JIT_MIN_ROWS rows or already compiled; default, the
+ * HK_JIT environment variable "0"/"1"/"auto" sets the initial mode).
+ * Returns the previous mode, or -1 for a bad mode. */
+#define HK_JIT_MIN_ROWS (1LL << 22)
+int hk_set_jit_mode(int32_t mode);
+/* programs specialised so far in this process (cache entries) */
+int64_t hk_jit_count(void);
+/* The CUDA source emitted for a program (into buf, NUL-terminated, at most
+ * cap bytes); returns the full length, -1 for a bad program. */
+int64_t hk_jit_source(const hk_program_t* f, char* buf, int64_t cap);
+/* NVRTC-compile a program for sm_100a without loading it (needs no GPU);
+ * *cubin_bytes = cubin size. */
+int hk_jit_compile(const hk_program_t* f, int64_t* cubin_bytes);
+
 /* Dalitz-plane integrands with a specialised (non-interpreted) device path:
  * s = m^2 of daughters i+j (0-based) in the op order of the reference's
  * pinned integrand (test_phasespace.py:196-201); f = s + 0.0 (identity) or a

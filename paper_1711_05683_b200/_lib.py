@@ -40,6 +40,7 @@ EXPORTS = (
     "hk_nll_partials", "hk_nll_eval", "hk_model_density",
     "hk_yield_partials", "hk_splot_weights",
     "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
+    "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
 )
 
 
@@ -124,6 +125,10 @@ _SIGS = {
     "hk_compact": (_INT, [_PP, _I32, _I64, _P, _P, _PP, _I32, _P]),
     "hk_scan_counts": (_INT, [_P, _I64, _P, _P, _P]),
     "hk_sample_pdf": (_INT, [_F, _I32, _PD, _PD, ctypes.c_double, _K, _U64, _I64, _I32, _PP, _P, _P]),
+    "hk_set_jit_mode": (_INT, [_I32]),
+    "hk_jit_count": (_I64, []),
+    "hk_jit_source": (_I64, [_F, ctypes.c_char_p, _I64]),
+    "hk_jit_compile": (_INT, [_F, ctypes.POINTER(_I64)]),
 }
 
 _lock = threading.Lock()
@@ -297,3 +302,49 @@ def fold(partials, n_parts: int, width: int):
     check(lib().hk_fold_partials(ptr(partials) if n_parts else None, int(n_parts), int(width),
                                  ptr(out), stream_ptr()), "hk_fold_partials")
     return out
+
+
+JIT_OFF, JIT_ALWAYS, JIT_AUTO = 0, 1, 2
+HK_JIT_MIN_ROWS = 1 << 22
+
+
+def set_jit_mode(mode: int) -> int:
+    """Functor specialisation policy (hk_set_jit_mode); returns the previous mode."""
+    prev = load_library().hk_set_jit_mode(int(mode))
+    if prev < 0:
+        raise ValueError(last_error())
+    return prev
+
+
+class jit_mode:
+    """``with jit_mode(JIT_OFF): ...`` -- scoped specialisation policy."""
+
+    def __init__(self, mode: int):
+        self.mode = mode
+        self.prev = None
+
+    def __enter__(self):
+        self.prev = set_jit_mode(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        set_jit_mode(self.prev)
+        return False
+
+
+def jit_source(program) -> str:
+    """CUDA source emitted for a lowered program (hk_jit_source)."""
+    L = load_library()
+    n = L.hk_jit_source(program, None, 0)
+    if n < 0:
+        raise ValueError(last_error())
+    buf = ctypes.create_string_buffer(n + 1)
+    L.hk_jit_source(program, buf, n + 1)
+    return buf.value.decode()
+
+
+def jit_compile(program) -> int:
+    """NVRTC-compile a program for sm_100a without a device; returns cubin bytes."""
+    out = ctypes.c_int64(0)
+    check(load_library().hk_jit_compile(program, ctypes.byref(out)), "hk_jit_compile")
+    return out.value

@@ -32,6 +32,23 @@ inline unsigned chunk_grid(int64_t chunks) {
   return (unsigned)(chunks < 1 ? 1 : (chunks > cap ? cap : chunks));
 }
 
+// hk_jit.cu: specialised functor kernels.  JitArgs is mirrored field for
+// field by the NVRTC-compiled source.
+constexpr int kJitMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
+constexpr int kJitMoments = 0;
+constexpr int kJitMap = 1;
+struct JitArgs {
+  const double* cols[kJitMaxCols];
+  long long count;
+  double* part;
+  unsigned long long* div0;
+  unsigned long long* nonfin;
+  double* out;
+};
+// *fn = specialised kernel for the program (kind kJitMoments / kJitMap), or
+// nullptr when the interpreter should run (mode / size policy).
+int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn);
+
 }  // namespace hk
 
 #define HK_REQUIRE(cond, ...)       \

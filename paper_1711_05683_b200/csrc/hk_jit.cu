@@ -1,0 +1,365 @@
+// hk_jit.cu -- runtime specialisation of functor programs.
+//
+// Hydra instantiates the user's functor into the kernel at C++ compile time.
+// The Python API receives functors at run time, so the device path lowers
+// them to an hk_program_t (functors.py:lower) which the interpreter in
+// hk_device.cuh runs op by op.  The interpreter is instruction-bound
+// (warp-uniform dispatch + local-memory slots, ~20 instructions per op); for
+// big blocks this file emits the program as straight-line CUDA, compiles it
+// with NVRTC for sm_100a and caches the cubin per program, so the average
+// over a stored block runs at HBM speed.
+//
+// Bit-identity with the interpreter: every operation is written with the
+// explicit round-to-nearest intrinsics in the interpreter's order, NVRTC runs
+// with --fmad=false (the interpreter's TU is built with -fmad=false), exp/log
+// come from the same libdevice, and the chunk moments use the same per-thread
+// order and the same block tree as k_moments / block_sum_store<5>.
+// tests/test_jit_gpu.py checks interpreter == specialised bitwise.
+//
+// NVRTC is dlopen'ed on first use, so the library keeps no link-time
+// dependency on it (the CPU ABI tests load the .so without a CUDA driver).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "hepkit_cuda.h"
+#include "hk_host.h"
+
+namespace hk {
+
+namespace {
+
+// ------------------------------------------------------------ NVRTC access --
+struct Nvrtc {
+  bool tried = false;
+  void* so = nullptr;
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  decltype(&nvrtcGetErrorString) err = nullptr;
+};
+
+template <class F>
+bool sym(void* so, const char* name, F* out) {
+  *out = reinterpret_cast<F>(dlsym(so, name));
+  return *out != nullptr;
+}
+
+// The toolkit's own NVRTC first (same libdevice as nvcc built the
+// interpreter with), then whatever the loader finds.
+bool load_nvrtc(Nvrtc& N) {
+  if (N.tried) return N.so != nullptr;
+  N.tried = true;
+  const char* names[] = {"/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12", "libnvrtc.so"};
+  for (const char* n : names) {
+    N.so = dlopen(n, RTLD_NOW | RTLD_LOCAL);
+    if (N.so) break;
+  }
+  if (!N.so) return false;
+  bool ok = sym(N.so, "nvrtcCreateProgram", &N.create) && sym(N.so, "nvrtcCompileProgram", &N.compile) &&
+            sym(N.so, "nvrtcGetCUBINSize", &N.cubin_size) && sym(N.so, "nvrtcGetCUBIN", &N.cubin) &&
+            sym(N.so, "nvrtcGetProgramLogSize", &N.log_size) && sym(N.so, "nvrtcGetProgramLog", &N.log) &&
+            sym(N.so, "nvrtcDestroyProgram", &N.destroy) && sym(N.so, "nvrtcGetErrorString", &N.err);
+  if (!ok) {
+    dlclose(N.so);
+    N.so = nullptr;
+  }
+  return ok;
+}
+
+// -------------------------------------------------------------- code emit --
+std::string hex_const(double v) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "__longlong_as_double(0x%016llxll)", (unsigned long long)bits);
+  return buf;
+}
+
+// Straight-line body of the program: one const double per op, slots renamed
+// to the op that last wrote them (the program is in execution order).
+std::string emit_function(const hk_program_t& P) {
+  std::string s;
+  s += "__device__ __forceinline__ double hk_f(const JitArgs& a, long long r, bool& d0) {\n";
+  int slot_of[HK_MAX_SLOTS];
+  for (int& x : slot_of) x = -1;
+  auto v = [&](int slot) -> std::string {
+    return slot_of[slot] < 0 ? std::string("0.0") : "v" + std::to_string(slot_of[slot]);
+  };
+  char line[512];
+  for (int i = 0; i < P.n_ops; ++i) {
+    const std::string A = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST ? "" : v(P.a[i]);
+    const std::string B = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST ? "" : v(P.b[i]);
+    const std::string c1 = hex_const(P.cst[i]), c2 = hex_const(P.cst2[i]);
+    std::string e;
+    switch (P.op[i]) {
+      case HK_OP_COL:
+        std::snprintf(line, sizeof(line), "__ldg(a.cols[%d] + r)", P.a[i]);
+        e = line;
+        break;
+      case HK_OP_CONST: e = c1; break;
+      case HK_OP_ADD: e = "__dadd_rn(" + A + ", " + B + ")"; break;
+      case HK_OP_SUB: e = "__dsub_rn(" + A + ", " + B + ")"; break;
+      case HK_OP_MUL: e = "__dmul_rn(" + A + ", " + B + ")"; break;
+      case HK_OP_DIV:
+        s += "  if (" + B + " == 0.0) d0 = true;\n";
+        e = "__ddiv_rn(" + A + ", " + B + ")";
+        break;
+      case HK_OP_NEG: e = "-" + A; break;
+      case HK_OP_SQRT: e = "__dsqrt_rn(" + A + ")"; break;
+      case HK_OP_EXP: e = "exp(" + A + ")"; break;
+      case HK_OP_LOG: e = "log(" + A + ")"; break;
+      case HK_OP_GAUSS:  // exp(-0.5 z z) / (s sqrt(2 pi)), z = (a - mu) / s
+        e = "__ddiv_rn(exp(__dmul_rn(__dmul_rn(-0.5, __ddiv_rn(__dsub_rn(" + A + ", " + c1 + "), " + c2 +
+            ")), __ddiv_rn(__dsub_rn(" + A + ", " + c1 + "), " + c2 + "))), __dmul_rn(" + c2 +
+            ", 2.5066282746310002))";
+        break;
+      case HK_OP_EXPO: e = "exp(__ddiv_rn(-" + A + ", " + c1 + "))"; break;
+      case HK_OP_BW:  // 1 / ((a - m0^2)^2 + m0^2 g0^2)
+        e = "__ddiv_rn(1.0, __dadd_rn(__dmul_rn(__dsub_rn(" + A + ", __dmul_rn(" + c1 + ", " + c1 +
+            ")), __dsub_rn(" + A + ", __dmul_rn(" + c1 + ", " + c1 + "))), __dmul_rn(__dmul_rn(" + c1 +
+            ", " + c1 + "), __dmul_rn(" + c2 + ", " + c2 + "))))";
+        break;
+      case HK_OP_ADD0: e = "__dadd_rn(" + A + ", 0.0)"; break;
+      case HK_OP_SQUARE: e = "__dmul_rn(" + A + ", " + A + ")"; break;
+      default: e = "__longlong_as_double(0x7ff8000000000000ll)"; break;
+    }
+    s += "  const double v" + std::to_string(i) + " = " + e + ";\n";
+    slot_of[P.dst[i]] = i;
+  }
+  s += "  return " + v(P.result) + ";\n}\n";
+  return s;
+}
+
+const char* kPrelude = R"(
+typedef unsigned long long u64;
+struct JitArgs {
+  const double* cols[HK_JIT_MAX_COLS];
+  long long count;
+  double* part;
+  u64* div0;
+  u64* nonfin;
+  double* out;
+};
+)";
+
+// Chunk moments: the per-thread order and block tree of k_moments /
+// block_sum_store<5> (hk_phsp.cu, hk_device.cuh).
+const char* kKernels = R"(
+extern "C" __global__ void __launch_bounds__(256) hk_jit_moments(const __grid_constant__ JitArgs a) {
+  __shared__ double sm[8][5];
+  const long long chunks = (a.count + 4095) / 4096;
+  for (long long c = blockIdx.x; c < chunks; c += gridDim.x) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const long long r = c * 4096 + i * 256 + threadIdx.x;
+      if (r < a.count) {
+        bool d0 = false;
+        const double f = hk_f(a, r, d0);
+        if (d0 && a.div0) atomicMin(a.div0, (u64)r);
+        if (!isfinite(f) && a.nonfin) atomicMin(a.nonfin, (u64)r);
+        const double w = __ldg(a.cols[0] + r);
+        const double ww = __dmul_rn(w, w);
+        acc[0] = __dadd_rn(acc[0], w);
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(w, f));
+        acc[2] = __dadd_rn(acc[2], ww);
+        acc[3] = __dadd_rn(acc[3], __dmul_rn(ww, f));
+        acc[4] = __dadd_rn(acc[4], __dmul_rn(__dmul_rn(ww, f), f));
+      }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int w = 0; w < 5; ++w) acc[w] = __dadd_rn(acc[w], __shfl_down_sync(0xffffffffu, acc[w], off));
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int w = 0; w < 5; ++w) sm[warp][w] = acc[w];
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+      double s = sm[0][threadIdx.x];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) s = __dadd_rn(s, sm[i][threadIdx.x]);
+      a.part[5 * c + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(256) hk_jit_map(const __grid_constant__ JitArgs a) {
+  const long long r = blockIdx.x * 256LL + threadIdx.x;
+  if (r >= a.count) return;
+  bool d0 = false;
+  a.out[r] = hk_f(a, r, d0);
+  if (d0 && a.div0) atomicMin(a.div0, (u64)r);
+}
+)";
+
+struct Entry {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern[2] = {nullptr, nullptr};
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, Entry> g_cache;
+Nvrtc g_nvrtc;
+int g_mode = -1;
+
+int initial_mode() {
+  const char* e = std::getenv("HK_JIT");
+  if (!e || !*e || !std::strcmp(e, "auto")) return 2;
+  if (!std::strcmp(e, "0")) return 0;
+  if (!std::strcmp(e, "1")) return 1;
+  return 2;
+}
+
+std::string program_key(const hk_program_t& P) {
+  std::string k;
+  k.reserve(8 + P.n_ops * 32);
+  auto put = [&](const void* p, size_t n) { k.append(reinterpret_cast<const char*>(p), n); };
+  put(&P.n_ops, 4);
+  put(&P.result, 4);
+  for (int i = 0; i < P.n_ops; ++i) {
+    put(&P.op[i], 4);
+    put(&P.dst[i], 4);
+    put(&P.a[i], 4);
+    put(&P.b[i], 4);
+    put(&P.cst[i], 8);
+    put(&P.cst2[i], 8);
+  }
+  return k;
+}
+
+std::string full_source(const hk_program_t& P) {
+  return "#define HK_JIT_MAX_COLS " + std::to_string(kJitMaxCols) + "\n" + kPrelude + emit_function(P) +
+         kKernels;
+}
+
+// NVRTC -> sm_100a cubin (no device needed)
+int compile_cubin(const hk_program_t& P, std::vector<char>* cubin) {
+  if (!load_nvrtc(g_nvrtc)) {
+    set_error("functor specialisation: NVRTC (libnvrtc.so.12) not loadable");
+    return HK_ECUDA;
+  }
+  Nvrtc& N = g_nvrtc;
+  const std::string src = full_source(P);
+  nvrtcProgram prog;
+  nvrtcResult rc = N.create(&prog, src.c_str(), "hk_functor.cu", 0, nullptr, nullptr);
+  if (rc != NVRTC_SUCCESS) {
+    set_error("nvrtcCreateProgram: %s", N.err(rc));
+    return HK_ECUDA;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo"};
+  rc = N.compile(prog, 4, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    N.log_size(prog, &n);
+    std::vector<char> log(n + 1, 0);
+    N.log(prog, log.data());
+    set_error("functor specialisation failed: %s: %.380s", N.err(rc), log.data());
+    N.destroy(&prog);
+    return HK_ECUDA;
+  }
+  size_t n = 0;
+  N.cubin_size(prog, &n);
+  cubin->resize(n);
+  N.cubin(prog, cubin->data());
+  N.destroy(&prog);
+  return HK_OK;
+}
+
+int compile_entry(const hk_program_t& P, Entry* out) {
+  std::vector<char> cubin;
+  if (int rc = compile_cubin(P, &cubin)) return rc;
+  HK_CUDA(cudaLibraryLoadData(&out->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMoments], out->lib, "hk_jit_moments"));
+  HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMap], out->lib, "hk_jit_map"));
+  return HK_OK;
+}
+
+}  // namespace
+
+int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn) {
+  *fn = nullptr;
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (g_mode < 0) g_mode = initial_mode();
+  if (g_mode == 0) return HK_OK;
+  const std::string key = program_key(P);
+  auto it = g_cache.find(key);
+  if (it == g_cache.end()) {
+    if (g_mode == 2 && rows < HK_JIT_MIN_ROWS) return HK_OK;  // small: the interpreter is cheaper
+    Entry e;
+    if (int rc = compile_entry(P, &e)) {
+      if (g_mode == 1) return rc;
+      g_mode = 0;  // auto: NVRTC unusable here, stay on the (GPU) interpreter
+      return HK_OK;
+    }
+    it = g_cache.emplace(key, e).first;
+  }
+  *fn = reinterpret_cast<const void*>(it->second.kern[kind]);
+  return HK_OK;
+}
+
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int hk_set_jit_mode(int32_t mode) {
+  if (mode < 0 || mode > 2) {
+    set_error("jit mode %d not in 0..2", mode);
+    return -1;
+  }
+  std::lock_guard<std::mutex> lock(g_mu);
+  const int prev = g_mode < 0 ? initial_mode() : g_mode;
+  g_mode = mode;
+  return prev;
+}
+
+int64_t hk_jit_source(const hk_program_t* f, char* buf, int64_t cap) {
+  if (!f || f->n_ops < 1 || f->n_ops > HK_MAX_PROGRAM) {
+    set_error("bad program");
+    return -1;
+  }
+  const std::string src = full_source(*f);
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>((size_t)cap - 1, src.size());
+    std::memcpy(buf, src.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)src.size();
+}
+
+int hk_jit_compile(const hk_program_t* f, int64_t* cubin_bytes) {
+  HK_REQUIRE(f && f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "bad program");
+  std::vector<char> cubin;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (int rc = compile_cubin(*f, &cubin)) return rc;
+  }
+  if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
+  return HK_OK;
+}
+
+int64_t hk_jit_count(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  return (int64_t)g_cache.size();
+}
+
+}  // extern "C"

@@ -288,6 +288,19 @@ __global__ void __launch_bounds__(kBlock) k_moments(const __grid_constant__ MomA
   }
 }
 
+static_assert(kJitMaxCols == kMaxCols, "JitArgs column capacity");
+
+inline JitArgs jit_args(const MomArgs& a) {
+  JitArgs j;
+  std::memset(&j, 0, sizeof(j));
+  for (int c = 0; c < a.n_cols; ++c) j.cols[c] = a.cols[c];
+  j.count = a.count;
+  j.part = a.part;
+  j.div0 = a.div0_bad;
+  j.nonfin = a.nonfinite_bad;
+  return j;
+}
+
 __global__ void __launch_bounds__(kBlock) k_map(const __grid_constant__ MomArgs a, double* out) {
   const int64_t r = blockIdx.x * (int64_t)kBlock + threadIdx.x;
   if (r >= a.count) return;
@@ -881,6 +894,15 @@ int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_coun
   // d_first_bad[0] = first zero divisor, d_first_bad[1] = first non-finite f
   a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
   a.nonfinite_bad = d_first_bad ? reinterpret_cast<unsigned long long*>(d_first_bad) + 1 : nullptr;
+  const void* jit = nullptr;
+  if (int rc = jit_kernel(*f, ev_count, kJitMoments, &jit)) return rc;
+  if (jit) {  // specialised straight-line program (hk_jit.cu), bit-identical
+    JitArgs j = jit_args(a);
+    void* args[] = {&j};
+    HK_CUDA(cudaLaunchKernel(jit, dim3(chunk_grid(num_chunks(ev_count))), dim3(kBlock), args, 0,
+                             as_stream(stream)));
+    return HK_OK;
+  }
   k_moments<<<chunk_grid(num_chunks(ev_count)), kBlock, 0, as_stream(stream)>>>(a);
   return check_launch("k_moments");
 }
@@ -902,6 +924,16 @@ int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const
   a.count = n;
   a.f = *f;
   a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  const void* jit = nullptr;
+  if (int rc = jit_kernel(*f, n, kJitMap, &jit)) return rc;
+  if (jit) {
+    JitArgs j = jit_args(a);
+    j.out = d_out;
+    void* args[] = {&j};
+    HK_CUDA(cudaLaunchKernel(jit, dim3((unsigned)((n + kBlock - 1) / kBlock)), dim3(kBlock), args, 0,
+                             as_stream(stream)));
+    return HK_OK;
+  }
   k_map<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, as_stream(stream)>>>(a, d_out);
   return check_launch("k_map");
 }

@@ -99,3 +99,24 @@ def m23sq_builder(cols):
     py = cols["p2_py"] + cols["p3_py"]
     pz = cols["p2_pz"] + cols["p3_pz"]
     return (e * e - px * px - py * py - pz * pz,)
+
+
+def jit_cases(hk):
+    """(name, expr, arg_builder) over the phase-space schema covering every
+    program opcode -- shared by the specialisation tests (host + GPU)."""
+    import numpy as np
+
+    mean, sigma, tau = hk.Parameter("mean", 3.0), hk.Parameter("sigma", 0.4), hk.Parameter("tau", 1.7)
+    return [
+        ("m12sq", hk.identity(), m12sq_builder),
+        ("bw_m23sq", hk.breit_wigner(0.89555, 0.0473), m23sq_builder),
+        ("gauss_e1", hk.shape_gaussian(mean, sigma), lambda c: (c["p1_e"],)),
+        ("expo_e3", hk.shape_exponential(tau), lambda c: (c["p3_e"],)),
+        ("product", hk.identity() * hk.identity(), m12sq_builder),
+        ("ratio", hk.identity(), lambda c: (c["p1_e"] / c["p2_pz"],)),
+        ("transcendental", hk.identity(),
+         lambda c: (np.log(c["p1_e"]) + np.sqrt(c["p2_e"]) * np.exp(-c["p3_e"]),)),
+        ("coordinate", hk.coordinate(1, 2), lambda c: (c["p1_e"], c["p2_px"])),
+        ("square_neg", hk.identity(), lambda c: (-(c["p1_px"] ** 2) - c["weight"],)),
+        ("constant", hk.constant(2.5), lambda c: (c["p1_e"],)),
+    ]
