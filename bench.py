@@ -367,6 +367,22 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     out["C5"] = {"workload": "1e10 B0->J/psi K pi events, fused generation + <m12^2> weighted average, "
                              f"strong scaling over {world} GPU(s), no event store",
                  "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu)}
+    # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
+    # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
+    expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
+    n5g = 1_000_000_000 // world
+
+    def c5g():
+        return hk.phsp_integrate(expr, spec, mother, n5g, hk.RngKey(1, 1), m12, row_offset=rank * n5g,
+                                 return_partials=True)
+
+    dt_jit = _timed(torch, c5g, 3, dist)
+    with _lib.jit_mode(_lib.JIT_OFF):
+        dt_int = _timed(torch, c5g, 1, dist)
+    out["C5_generic"] = {"workload": "1e9 events, fused generation + <m12^2 * BW(m12^2)> (non-Dalitz-pair "
+                                     f"integrand) over {world} GPU(s)",
+                         "value": world * n5g / dt_jit, "unit": "events/s", "seconds": dt_jit,
+                         "interpreter_value": world * n5g / dt_int}
     return out
 
 

@@ -25,8 +25,10 @@
 #ifndef HEPKIT_CUDA_H
 #define HEPKIT_CUDA_H
 
+#ifndef __CUDACC_RTC__ /* NVRTC (hk_jit.cu) supplies the fixed-width types */
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -208,11 +210,15 @@ int hk_set_jit_mode(int32_t mode);
 /* programs specialised so far in this process (cache entries) */
 int64_t hk_jit_count(void);
 /* The CUDA source emitted for a program (into buf, NUL-terminated, at most
- * cap bytes); returns the full length, -1 for a bad program. */
-int64_t hk_jit_source(const hk_program_t* f, char* buf, int64_t cap);
-/* NVRTC-compile a program for sm_100a without loading it (needs no GPU);
+ * cap bytes); returns the full length, -1 for a bad program/target.
+ * n_daughters = 0: the stored-block module (hk_phsp_moments / hk_map_program);
+ * 2..8: the fused generate+integrate module (hk_phsp_integrate) for that
+ * final state and rng_mode (HK_RNG_*). */
+int64_t hk_jit_source(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, char* buf,
+                      int64_t cap);
+/* NVRTC-compile that module for sm_100a without loading it (needs no GPU);
  * *cubin_bytes = cubin size. */
-int hk_jit_compile(const hk_program_t* f, int64_t* cubin_bytes);
+int hk_jit_compile(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, int64_t* cubin_bytes);
 
 /* Dalitz-plane integrands with a specialised (non-interpreted) device path:
  * s = m^2 of daughters i+j (0-based) in the op order of the reference's

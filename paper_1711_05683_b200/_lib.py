@@ -127,8 +127,8 @@ _SIGS = {
     "hk_sample_pdf": (_INT, [_F, _I32, _PD, _PD, ctypes.c_double, _K, _U64, _I64, _I32, _PP, _P, _P]),
     "hk_set_jit_mode": (_INT, [_I32]),
     "hk_jit_count": (_I64, []),
-    "hk_jit_source": (_I64, [_F, ctypes.c_char_p, _I64]),
-    "hk_jit_compile": (_INT, [_F, ctypes.POINTER(_I64)]),
+    "hk_jit_source": (_I64, [_F, _I32, _I32, ctypes.c_char_p, _I64]),
+    "hk_jit_compile": (_INT, [_F, _I32, _I32, ctypes.POINTER(_I64)]),
 }
 
 _lock = threading.Lock()
@@ -332,19 +332,21 @@ class jit_mode:
         return False
 
 
-def jit_source(program) -> str:
-    """CUDA source emitted for a lowered program (hk_jit_source)."""
+def jit_source(program, n_daughters: int = 0, rng_mode: int = HK_RNG_REFERENCE) -> str:
+    """CUDA source emitted for a lowered program (hk_jit_source): the
+    stored-block module (n_daughters 0) or the fused generate+integrate one."""
     L = load_library()
-    n = L.hk_jit_source(program, None, 0)
+    n = L.hk_jit_source(program, n_daughters, rng_mode, None, 0)
     if n < 0:
         raise ValueError(last_error())
     buf = ctypes.create_string_buffer(n + 1)
-    L.hk_jit_source(program, buf, n + 1)
+    L.hk_jit_source(program, n_daughters, rng_mode, buf, n + 1)
     return buf.value.decode()
 
 
-def jit_compile(program) -> int:
-    """NVRTC-compile a program for sm_100a without a device; returns cubin bytes."""
+def jit_compile(program, n_daughters: int = 0, rng_mode: int = HK_RNG_REFERENCE) -> int:
+    """NVRTC-compile a module for sm_100a without a device; returns cubin bytes."""
     out = ctypes.c_int64(0)
-    check(load_library().hk_jit_compile(program, ctypes.byref(out)), "hk_jit_compile")
+    check(load_library().hk_jit_compile(program, n_daughters, rng_mode, ctypes.byref(out)),
+          "hk_jit_compile")
     return out.value

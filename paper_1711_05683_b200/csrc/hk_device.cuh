@@ -14,7 +14,9 @@
 //    <~1e-16 * E (the parity tolerance is 1e-12 * E_daughter).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 #include "hepkit_cuda.h"
 #include "hk_math.cuh"

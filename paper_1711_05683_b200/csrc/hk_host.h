@@ -48,6 +48,8 @@ struct JitArgs {
 // *fn = specialised kernel for the program (kind kJitMoments / kJitMap), or
 // nullptr when the interpreter should run (mode / size policy).
 int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn);
+// same for the fused generate+integrate kernel (n daughters, RNG mode)
+int jit_integrate(const hk_program_t& P, int n, int mode, int64_t rows, const void** fn);
 
 }  // namespace hk
 

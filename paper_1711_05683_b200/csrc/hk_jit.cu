@@ -88,26 +88,29 @@ std::string hex_const(double v) {
   return buf;
 }
 
-// Straight-line body of the program: one const double per op, slots renamed
-// to the op that last wrote them (the program is in execution order).
-std::string emit_function(const hk_program_t& P) {
+// Straight-line program: one const double per op, slots renamed to the op
+// that last wrote them (the program is in execution order).  Column c reads
+// HBM (stored block) or the register-resident event (fused: c = 0 is the
+// weight w, c = 1 + 4 j + k is p[4 j + k]).  Zero divisors set d0.
+std::string emit_body(const hk_program_t& P, bool fused) {
   std::string s;
-  s += "__device__ __forceinline__ double hk_f(const JitArgs& a, long long r, bool& d0) {\n";
   int slot_of[HK_MAX_SLOTS];
   for (int& x : slot_of) x = -1;
   auto v = [&](int slot) -> std::string {
     return slot_of[slot] < 0 ? std::string("0.0") : "v" + std::to_string(slot_of[slot]);
   };
-  char line[512];
   for (int i = 0; i < P.n_ops; ++i) {
-    const std::string A = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST ? "" : v(P.a[i]);
-    const std::string B = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST ? "" : v(P.b[i]);
+    const bool leaf = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST;
+    const std::string A = leaf ? "" : v(P.a[i]);
+    const std::string B = leaf ? "" : v(P.b[i]);
     const std::string c1 = hex_const(P.cst[i]), c2 = hex_const(P.cst2[i]);
     std::string e;
     switch (P.op[i]) {
       case HK_OP_COL:
-        std::snprintf(line, sizeof(line), "__ldg(a.cols[%d] + r)", P.a[i]);
-        e = line;
+        if (fused)
+          e = P.a[i] == 0 ? std::string("w") : "p[" + std::to_string(P.a[i] - 1) + "]";
+        else
+          e = "__ldg(a.cols[" + std::to_string(P.a[i]) + "] + r)";
         break;
       case HK_OP_CONST: e = c1; break;
       case HK_OP_ADD: e = "__dadd_rn(" + A + ", " + B + ")"; break;
@@ -139,11 +142,12 @@ std::string emit_function(const hk_program_t& P) {
     s += "  const double v" + std::to_string(i) + " = " + e + ";\n";
     slot_of[P.dst[i]] = i;
   }
-  s += "  return " + v(P.result) + ";\n}\n";
+  s += "  return " + v(P.result) + ";\n";
   return s;
 }
 
-const char* kPrelude = R"(
+// ---- stored-block module: chunk moments + per-row map over HBM columns ----
+const char* kStoredPrelude = R"(
 typedef unsigned long long u64;
 struct JitArgs {
   const double* cols[HK_JIT_MAX_COLS];
@@ -157,7 +161,7 @@ struct JitArgs {
 
 // Chunk moments: the per-thread order and block tree of k_moments /
 // block_sum_store<5> (hk_phsp.cu, hk_device.cuh).
-const char* kKernels = R"(
+const char* kStoredKernels = R"(
 extern "C" __global__ void __launch_bounds__(256) hk_jit_moments(const __grid_constant__ JitArgs a) {
   __shared__ double sm[8][5];
   const long long chunks = (a.count + 4095) / 4096;
@@ -210,6 +214,60 @@ extern "C" __global__ void __launch_bounds__(256) hk_jit_map(const __grid_consta
 }
 )";
 
+// ---- fused module: the generator of hk_integrate.cuh with the program inlined
+// (LP64 fixed-width types: NVRTC has no libc headers)
+const char* kFusedPrelude = R"(
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long int64_t;
+typedef unsigned long uint64_t;
+typedef unsigned long size_t;
+#define UINT64_MAX 0xffffffffffffffffUL
+#include "hk_integrate.cuh"
+)";
+
+struct EmbeddedHeader {
+  const char* name;
+  const char* text;
+};
+const EmbeddedHeader kHeaders[] = {
+#include "build/hk_embed.inc"
+};
+constexpr int kNumHeaders = sizeof(kHeaders) / sizeof(kHeaders[0]);
+
+// n == 0: stored-block module; else fused generate+integrate for n daughters
+std::string full_source(const hk_program_t& P, int n, int mode) {
+  if (n == 0)
+    return "#define HK_JIT_MAX_COLS " + std::to_string(kJitMaxCols) + "\n" + kStoredPrelude +
+           "__device__ __forceinline__ double hk_f(const JitArgs& a, long long r, bool& d0) {\n" +
+           emit_body(P, false) + "}\n" + kStoredKernels;
+  const std::string N = std::to_string(n), M = std::to_string(mode);
+  return std::string(kFusedPrelude) +
+         "namespace hk {\n"
+         "struct JitIntegrand {\n"
+         "  static constexpr bool kIlp2 = true;\n"
+         "  template <int N>\n"
+         "  __device__ __forceinline__ static double eval(const IntArgs& a, double w,\n"
+         "                                                const double (&p)[4 * N], uint64_t row) {\n"
+         "    bool d0 = false;\n"
+         "    const double f = [&]() {\n" +
+         emit_body(P, true) +
+         "    }();\n"
+         "    if (d0) record_bad(a.div0_bad, row);\n"
+         "    return f;\n"
+         "  }\n"
+         "};\n"
+         "}  // namespace hk\n"
+         "extern \"C\" __global__ void __launch_bounds__(256, hk::GenShape<" + N + ">::min_blocks)\n"
+         "    hk_jit_integrate(const __grid_constant__ hk::IntArgs a) {\n"
+         "  hk::integrate_chunks<" + N + ", " + M + ", hk::JitIntegrand>(a);\n"
+         "}\n";
+}
+
 struct Entry {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern[2] = {nullptr, nullptr};
@@ -228,10 +286,12 @@ int initial_mode() {
   return 2;
 }
 
-std::string program_key(const hk_program_t& P) {
+std::string cache_key(const hk_program_t& P, int n, int mode) {
   std::string k;
-  k.reserve(8 + P.n_ops * 32);
-  auto put = [&](const void* p, size_t n) { k.append(reinterpret_cast<const char*>(p), n); };
+  k.reserve(16 + P.n_ops * 32);
+  auto put = [&](const void* p, size_t b) { k.append(reinterpret_cast<const char*>(p), b); };
+  put(&n, 4);
+  put(&mode, 4);
   put(&P.n_ops, 4);
   put(&P.result, 4);
   for (int i = 0; i < P.n_ops; ++i) {
@@ -245,74 +305,89 @@ std::string program_key(const hk_program_t& P) {
   return k;
 }
 
-std::string full_source(const hk_program_t& P) {
-  return "#define HK_JIT_MAX_COLS " + std::to_string(kJitMaxCols) + "\n" + kPrelude + emit_function(P) +
-         kKernels;
-}
-
 // NVRTC -> sm_100a cubin (no device needed)
-int compile_cubin(const hk_program_t& P, std::vector<char>* cubin) {
+int compile_cubin(const hk_program_t& P, int n, int mode, std::vector<char>* cubin) {
   if (!load_nvrtc(g_nvrtc)) {
     set_error("functor specialisation: NVRTC (libnvrtc.so.12) not loadable");
     return HK_ECUDA;
   }
   Nvrtc& N = g_nvrtc;
-  const std::string src = full_source(P);
+  const std::string src = full_source(P, n, mode);
+  const char* names[kNumHeaders];
+  const char* texts[kNumHeaders];
+  for (int h = 0; h < kNumHeaders; ++h) {
+    names[h] = kHeaders[h].name;
+    texts[h] = kHeaders[h].text;
+  }
   nvrtcProgram prog;
-  nvrtcResult rc = N.create(&prog, src.c_str(), "hk_functor.cu", 0, nullptr, nullptr);
+  nvrtcResult rc = N.create(&prog, src.c_str(), "hk_functor.cu", kNumHeaders, texts, names);
   if (rc != NVRTC_SUCCESS) {
     set_error("nvrtcCreateProgram: %s", N.err(rc));
     return HK_ECUDA;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo"};
-  rc = N.compile(prog, 4, opts);
+  // -default-device: the headers' unannotated inline helpers become device code
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
+                        "-default-device"};
+  rc = N.compile(prog, 5, opts);
   if (rc != NVRTC_SUCCESS) {
-    size_t n = 0;
-    N.log_size(prog, &n);
-    std::vector<char> log(n + 1, 0);
+    size_t len = 0;
+    N.log_size(prog, &len);
+    std::vector<char> log(len + 1, 0);
     N.log(prog, log.data());
     set_error("functor specialisation failed: %s: %.380s", N.err(rc), log.data());
     N.destroy(&prog);
     return HK_ECUDA;
   }
-  size_t n = 0;
-  N.cubin_size(prog, &n);
-  cubin->resize(n);
+  size_t len = 0;
+  N.cubin_size(prog, &len);
+  cubin->resize(len);
   N.cubin(prog, cubin->data());
   N.destroy(&prog);
   return HK_OK;
 }
 
-int compile_entry(const hk_program_t& P, Entry* out) {
+int compile_entry(const hk_program_t& P, int n, int mode, Entry* out) {
   std::vector<char> cubin;
-  if (int rc = compile_cubin(P, &cubin)) return rc;
+  if (int rc = compile_cubin(P, n, mode, &cubin)) return rc;
   HK_CUDA(cudaLibraryLoadData(&out->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-  HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMoments], out->lib, "hk_jit_moments"));
-  HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMap], out->lib, "hk_jit_map"));
+  if (n == 0) {
+    HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMoments], out->lib, "hk_jit_moments"));
+    HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMap], out->lib, "hk_jit_map"));
+  } else {
+    HK_CUDA(cudaLibraryGetKernel(&out->kern[0], out->lib, "hk_jit_integrate"));
+  }
   return HK_OK;
 }
 
-}  // namespace
-
-int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn) {
+int lookup(const hk_program_t& P, int n, int mode, int64_t rows, int slot, const void** fn) {
   *fn = nullptr;
   std::lock_guard<std::mutex> lock(g_mu);
   if (g_mode < 0) g_mode = initial_mode();
   if (g_mode == 0) return HK_OK;
-  const std::string key = program_key(P);
+  const std::string key = cache_key(P, n, mode);
   auto it = g_cache.find(key);
   if (it == g_cache.end()) {
     if (g_mode == 2 && rows < HK_JIT_MIN_ROWS) return HK_OK;  // small: the interpreter is cheaper
     Entry e;
-    if (int rc = compile_entry(P, &e)) {
+    if (int rc = compile_entry(P, n, mode, &e)) {
       if (g_mode == 1) return rc;
       g_mode = 0;  // auto: NVRTC unusable here, stay on the (GPU) interpreter
       return HK_OK;
     }
     it = g_cache.emplace(key, e).first;
   }
-  *fn = reinterpret_cast<const void*>(it->second.kern[kind]);
+  *fn = reinterpret_cast<const void*>(it->second.kern[slot]);
   return HK_OK;
+}
+
+}  // namespace
+
+int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn) {
+  return lookup(P, 0, 0, rows, kind, fn);
+}
+
+int jit_integrate(const hk_program_t& P, int n, int mode, int64_t rows, const void** fn) {
+  return lookup(P, n, mode, rows, 0, fn);
 }
 
 }  // namespace hk
@@ -332,12 +407,14 @@ int hk_set_jit_mode(int32_t mode) {
   return prev;
 }
 
-int64_t hk_jit_source(const hk_program_t* f, char* buf, int64_t cap) {
-  if (!f || f->n_ops < 1 || f->n_ops > HK_MAX_PROGRAM) {
-    set_error("bad program");
+int64_t hk_jit_source(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, char* buf,
+                      int64_t cap) {
+  if (!f || f->n_ops < 1 || f->n_ops > HK_MAX_PROGRAM || n_daughters < 0 || n_daughters > 8 ||
+      n_daughters == 1 || rng_mode < 0 || rng_mode > 1) {
+    set_error("bad program / target");
     return -1;
   }
-  const std::string src = full_source(*f);
+  const std::string src = full_source(*f, n_daughters, rng_mode);
   if (buf && cap > 0) {
     const size_t n = std::min<size_t>((size_t)cap - 1, src.size());
     std::memcpy(buf, src.data(), n);
@@ -346,12 +423,14 @@ int64_t hk_jit_source(const hk_program_t* f, char* buf, int64_t cap) {
   return (int64_t)src.size();
 }
 
-int hk_jit_compile(const hk_program_t* f, int64_t* cubin_bytes) {
+int hk_jit_compile(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, int64_t* cubin_bytes) {
   HK_REQUIRE(f && f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "bad program");
+  HK_REQUIRE(n_daughters == 0 || (n_daughters >= 2 && n_daughters <= 8), "n_daughters %d", n_daughters);
+  HK_REQUIRE(rng_mode == HK_RNG_REFERENCE || rng_mode == HK_RNG_PHILOX, "rng mode %d", rng_mode);
   std::vector<char> cubin;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    if (int rc = compile_cubin(*f, &cubin)) return rc;
+    if (int rc = compile_cubin(*f, n_daughters, rng_mode, &cubin)) return rc;
   }
   if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   return HK_OK;

@@ -19,9 +19,11 @@
 //             0/inf beyond; NaN propagates.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#endif
 
 #if defined(__CUDACC__)
 #define HK_HD __host__ __device__ __forceinline__

@@ -14,31 +14,12 @@
 #include "hepkit_cuda.h"
 #include "hk_device.cuh"
 #include "hk_host.h"
+#include "hk_integrate.cuh"
 
 namespace hk {
 
 constexpr int kMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
 constexpr int kFastMaxN = 8;  // templated register-resident kernels for n <= 8
-
-// Generator shape, measured on B200 for 1e8 3-body events (tools/bench_gen.py):
-//   1 event/iteration, 2 CTAs/SM (<=128 regs) ........ 2.55 ms
-//   1 event/iteration, 3 CTAs/SM (<=80 regs) ......... 2.315 ms
-//   2 events/iteration, 2 CTAs/SM (<=128 regs) ....... 2.240 ms  <- n <= 4
-//   2 events/iteration, 1 CTA/SM ..................... 2.747 ms
-// Two independent events per iteration give the scheduler interleavable
-// dependency chains (the kernel is issue/FP64-latency bound, "wait" stalls);
-// larger final states would spill and keep one event per iteration.
-template <int N>
-struct GenShape {
-  static constexpr int ilp = N <= 4 ? 2 : 1;
-  static constexpr int min_blocks = 2;
-};
-
-// fused integration (no stores), one event per iteration: 3 CTAs/SM for n <= 4
-template <int N>
-struct GenMinBlocks {
-  static constexpr int value = N <= 4 ? 3 : 2;
-};
 
 struct GenArgs {
   hk_decay_t d;
@@ -138,116 +119,14 @@ __global__ void __launch_bounds__(kBlock) k_generate_rt(const __grid_constant__ 
 }
 
 // ---------------------------------------------------- fused integration ----
-struct IntArgs {
-  hk_decay_t d;
-  RngParams rp;
-  uint64_t ev_begin;
-  int64_t count;
-  hk_program_t f;
-  double* part;  // 5 doubles per chunk
-  unsigned long long* div0_bad;
-  unsigned long long* nonfinite_bad;
-  hk_pair_integrand_t pair;  // kind != HK_PAIR_NONE: f from the fast pair-mass path
-};
-
-// daughter q's component c of the register-resident event, q a runtime index
-template <int N>
-__device__ __forceinline__ double pick(const double (&p)[4 * N], int q, int c) {
-  double v = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) v = select_f64(j == q, p[4 * j + c], v);
-  return v;
-}
-
-// m^2 of daughters i+j with the op order of the reference's pinned integrand
-// (test_phasespace.py:196-201), then identity (+0.0) or a Breit-Wigner.
-template <int N>
-__device__ __forceinline__ double pair_integrand(const double (&p)[4 * N],
-                                                 const hk_pair_integrand_t& f) {
-  const double e = pick<N>(p, f.i, 0) + pick<N>(p, f.j, 0);
-  const double x = pick<N>(p, f.i, 1) + pick<N>(p, f.j, 1);
-  const double y = pick<N>(p, f.i, 2) + pick<N>(p, f.j, 2);
-  const double z = pick<N>(p, f.i, 3) + pick<N>(p, f.j, 3);
-  const double s = e * e - x * x - y * y - z * z;
-  if (f.kind == HK_PAIR_BW) {
-    const double t = s - f.m0 * f.m0;
-    return 1.0 / (t * t + (f.m0 * f.m0) * (f.g0 * f.g0));
-  }
-  return s + 0.0;
-}
-
-// phsp_generate -> phsp_average (phasespace.py:162-188 then :310-349) with the
-// event kept in registers: 0 bytes of HBM per event.
+// (chunk loop and integrand policies in hk_integrate.cuh)
 template <int N, int MODE, bool PAIR>
 __global__ void __launch_bounds__(kBlock, PAIR ? GenShape<N>::min_blocks : 1)
     k_integrate(const __grid_constant__ IntArgs a) {
-  const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
-  Frame mf{};
-  if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
-                                  a.d.m_mother);
-  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (PAIR && GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
-#pragma unroll 1
-      for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
-        const uint64_t row0 = a.ev_begin + (uint64_t)(c * HK_CHUNK + i * kBlock + threadIdx.x);
-        const uint64_t row1 = row0 + HK_CHUNK / 2;
-        double p0[4 * N], p1[4 * N];
-        const double w0 = rest_event<N, MODE>(a.d, a.rp, row0, p0);
-        const double w1 = rest_event<N, MODE>(a.d, a.rp, row1, p1);
-        const double f0 = pair_integrand<N>(p0, a.pair);
-        const double f1 = pair_integrand<N>(p1, a.pair);
-        if (!isfinite(f0)) record_bad(a.nonfinite_bad, row0);
-        if (!isfinite(f1)) record_bad(a.nonfinite_bad, row1);
-        const double ww0 = w0 * w0, ww1 = w1 * w1;
-        acc[0] += w0;
-        acc[1] += w0 * f0;
-        acc[2] += ww0;
-        acc[3] += ww0 * f0;
-        acc[4] += ww0 * f0 * f0;
-        acc[0] += w1;
-        acc[1] += w1 * f1;
-        acc[2] += ww1;
-        acc[3] += ww1 * f1;
-        acc[4] += ww1 * f1 * f1;
-      }
-      block_sum_store<5>(acc, a.part + 5 * c);
-      continue;
-    }
-#pragma unroll 1
-    for (int i = 0; i < kRowsPerThread; ++i) {
-      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
-      if (r < a.count) {
-        const uint64_t row = a.ev_begin + (uint64_t)r;
-        double v[4 * N + 1];
-        double p[4 * N];
-        const double w = rest_event<N, MODE>(a.d, a.rp, row, p);
-        if (a.d.moving) {
-#pragma unroll
-          for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
-        }
-        double f;
-        if (PAIR) {
-          f = pair_integrand<N>(p, a.pair);
-        } else {
-          v[0] = w;
-#pragma unroll
-          for (int j = 0; j < 4 * N; ++j) v[1 + j] = p[j];
-          bool div0 = false;
-          f = run_program(a.f, [&](int col) { return v[col]; }, &div0);
-          if (div0) record_bad(a.div0_bad, row);
-        }
-        if (!isfinite(f)) record_bad(a.nonfinite_bad, row);
-        const double ww = w * w;
-        acc[0] += w;
-        acc[1] += w * f;
-        acc[2] += ww;
-        acc[3] += ww * f;
-        acc[4] += ww * f * f;
-      }
-    }
-    block_sum_store<5>(acc, a.part + 5 * c);
-  }
+  if constexpr (PAIR)
+    integrate_chunks<N, MODE, PairIntegrand>(a);
+  else
+    integrate_chunks<N, MODE, ProgramIntegrand>(a);
 }
 
 // ------------------------------------------- moments over stored columns ---
@@ -961,15 +840,25 @@ int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_b
   a.rp = make_rng(*key);
   a.ev_begin = ev_begin;
   a.count = ev_count;
-  if (fast)
-    a.pair = *pair;
-  else
-    a.f = *f;
+  // a recognised pair integrand also arrives with its program (the Python
+  // side always lowers it): the specialised kernel serves both
+  const bool have_prog = f != nullptr && (!fast || validate_program(f, 4 * spec->n + 1) == HK_OK);
+  if (fast) a.pair = *pair;
+  if (have_prog) a.f = *f;
   a.part = d_partials;
   a.div0_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
   a.nonfinite_bad = d_first_bad ? reinterpret_cast<unsigned long long*>(d_first_bad) + 1 : nullptr;
   const unsigned grid = chunk_grid(num_chunks(ev_count));
   cudaStream_t st = as_stream(stream);
+  if (have_prog && spec->n <= kFastMaxN) {  // specialised generator + straight-line integrand (hk_jit.cu)
+    const void* jit = nullptr;
+    if (int rc = jit_integrate(*f, spec->n, key->mode, ev_count, &jit)) return rc;
+    if (jit) {
+      void* args[] = {&a};
+      HK_CUDA(cudaLaunchKernel(jit, dim3(grid), dim3(kBlock), args, 0, st));
+      return HK_OK;
+    }
+  }
   return key->mode == HK_RNG_REFERENCE ? dispatch_integrate<HK_RNG_REFERENCE>(a, grid, st)
                                        : dispatch_integrate<HK_RNG_PHILOX>(a, grid, st);
 }

@@ -94,3 +94,27 @@ def test_auto_policy(hk, cuda):
     with _lib.jit_mode(_lib.JIT_OFF):
         r_big_interp = hk.phsp_average(expr, big, m12sq_builder)
     assert r_big.value == r_big_interp.value and r_big.error == r_big_interp.error
+
+
+@pytest.mark.parametrize("n_daughters,rng,moving", [(3, "reference", False), (3, "philox", False),
+                                                    (3, "reference", True), (5, "reference", False)])
+def test_fused_integrate_bitwise(hk, cuda, n_daughters, rng, moving):
+    """phsp_integrate: specialised generator+integrand == interpreter, chunk
+    moments bit for bit (ragged tail chunk included)."""
+    import torch
+    from paper_1711_05683_b200 import _lib
+    masses = (0.5, 0.3, 0.2, 0.1, 0.15)[:n_daughters]
+    spec = hk.DecaySpec(B0_MASS, masses)
+    mother = (hk.FourVector(float(np.hypot(B0_MASS, 3.0)), 1.0, -2.0, 2.0) if moving
+              else hk.FourVector.at_rest(B0_MASS))
+    n = 7 * 4096 + 1234
+    for name, expr, builder in jit_cases(hk):
+        def run():
+            return hk.phsp_integrate(expr, spec, mother, n, hk.RngKey(4, 9), builder, rng=rng,
+                                     return_partials=True)
+        with _lib.jit_mode(_lib.JIT_OFF):
+            ref = _bits(run())
+        with _lib.jit_mode(_lib.JIT_ALWAYS):
+            got = _bits(run())
+        assert np.array_equal(got, ref), (name, n_daughters, rng, moving)
+        torch.cuda.synchronize()

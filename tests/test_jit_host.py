@@ -64,3 +64,18 @@ def test_mode_switch_and_validation(hk):
     finally:
         _lib.set_jit_mode(prev)
     assert _lib.load_library().hk_jit_count() >= 0
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="NVRTC not in this image")
+def test_fused_generator_module_compiles(hk):
+    """The fused generate+integrate module: the embedded device headers compile
+    under NVRTC for every templated final state and both RNG modes."""
+    from paper_1711_05683_b200 import _lib
+    progs = dict(_programs(hk))
+    src = _lib.jit_source(progs["transcendental"], 3, _lib.HK_RNG_REFERENCE)
+    assert "integrate_chunks<3, 0, hk::JitIntegrand>" in src
+    assert "__ldg" not in src.split("struct JitIntegrand")[1]      # event from registers, not HBM
+    for n, mode in ((2, 0), (3, 0), (3, 1), (8, 1)):
+        assert _lib.jit_compile(progs["gauss_e1"], n, mode) > 1000, (n, mode)
+    with pytest.raises(ValueError):
+        _lib.jit_compile(progs["gauss_e1"], 9, 0)
