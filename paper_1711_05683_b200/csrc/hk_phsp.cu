@@ -7,6 +7,7 @@
 // chunk in 16 row-strided steps so every column store is a fully coalesced
 // 256 B warp transaction, and the chunk's moment partial is a fixed-order
 // CTA reduction -- the GPU analogue of the reference's chunk partials.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -17,6 +18,8 @@
 #include "hk_integrate.cuh"
 
 namespace hk {
+
+namespace cg = cooperative_groups;
 
 constexpr int kMaxCols = 4 * HK_MAX_DAUGHTERS + 1;
 constexpr int kFastMaxN = 8;  // templated register-resident kernels for n <= 8
@@ -476,15 +479,27 @@ __global__ void k_rng(RngParams rp, const uint64_t* ctr, int64_t n, uint64_t* ra
 }
 
 // ----------------------------------------------------------------- folds ---
-// Deterministic fold: thread t sums parts t, t+1024, ... in order, then a
-// fixed shuffle/smem tree.  Same n_parts -> same bits, whatever produced them.
-__global__ void __launch_bounds__(1024) k_fold(const double* parts, int64_t n, int width,
-                                               double* out) {
-  __shared__ double sm[32][32];
+// Deterministic fold over one thread-block cluster of kFoldCtas CTAs: global
+// thread g sums parts g, g + 8192, ... in order, a fixed shuffle/smem tree
+// per CTA, then CTA 0 adds the CTAs' sums in rank order through distributed
+// shared memory.  One launch, no global scratch, 8 SMs of load bandwidth;
+// same n_parts -> same bits, whatever produced them.
+constexpr int kFoldCtas = 8;  // portable cluster size
+constexpr int kFoldThreads = 1024;
+
+__global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads)
+    k_fold(const double* parts, int64_t n, int width, double* out) {
+  __shared__ double sm[32][32];  // [warp][w]
+  __shared__ double cta_sum[32];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t g = (int64_t)rank * kFoldThreads + threadIdx.x;
+  constexpr int64_t stride = (int64_t)kFoldCtas * kFoldThreads;
   for (int w = 0; w < width; ++w) {
     double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += 1024) s += parts[i * width + w];
+#pragma unroll 4
+    for (int64_t i = g; i < n; i += stride) s += __ldg(parts + i * width + w);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
     if (lane == 0) sm[warp][w] = s;
@@ -493,12 +508,19 @@ __global__ void __launch_bounds__(1024) k_fold(const double* parts, int64_t n, i
   if (threadIdx.x < width) {
     double s = sm[0][threadIdx.x];
     for (int k = 1; k < 32; ++k) s += sm[k][threadIdx.x];
+    cta_sum[threadIdx.x] = s;
+  }
+  cl.sync();
+  if (rank == 0 && threadIdx.x < width) {
+    double s = cta_sum[threadIdx.x];
+    for (int r = 1; r < kFoldCtas; ++r) s += cl.map_shared_rank(cta_sum, r)[threadIdx.x];
     out[threadIdx.x] = s;
   }
+  cl.sync();  // remote shared memory stays live until CTA 0 has read it
 }
 
 int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStream_t st) {
-  k_fold<<<1, 1024, 0, st>>>(parts, n, width, out);
+  k_fold<<<kFoldCtas, kFoldThreads, 0, st>>>(parts, n, width, out);
   return check_launch("k_fold");
 }
 
