@@ -7,9 +7,11 @@
 // density -> positivity check -> log -> fixed-order CTA sum per 4096-row
 // chunk.  The per-component constants are folded on the host
 // (A_k = N_k / (sigma_k sqrt(2 pi) norm_k), 1/sigma_k, -1/tau_k), which moves a
-// density by a few ulp -- far inside the 1e-10 FCN tolerance -- and leaves
-// two exp, one log and ~12 DFMA-class ops per event: FP64-pipe bound, with
-// the 8 B/event column usually L2-resident (1e7 events = 80 MB < 126 MB L2).
+// density by a few ulp -- far inside the 1e-10 FCN tolerance.  For the
+// Gaussian + exponential model the density is factored as e^M * s
+// (density_factored): one exp per event, one log per 16 events, ~35 FP64
+// instructions per event -- FP64-pipe bound, with the 8 B/event column
+// usually L2-resident (1e7 events = 80 MB < 126 MB L2).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -27,7 +29,15 @@ struct Coeffs {
   double amp[HK_MAX_COMPONENTS];    // gauss: N/(s*sqrt(2pi)*norm); expo: N/norm
   double shift[HK_MAX_COMPONENTS];  // gauss: mean
   double scale[HK_MAX_COMPONENTS];  // gauss: 1/sigma; expo: -1/tau
+  // factored Gaussian+exponential path (kFcnFactored): exponents M inside
+  // (m_lo, m_hi) give amp_k e^M a normal, finite double for both k
+  double m_lo, m_hi;
 };
+
+// FCN kernel variants
+constexpr int kFcnGeneric = 0;   // any component list
+constexpr int kFcnGE = 1;        // Gaussian + exponential, reference op order
+constexpr int kFcnFactored = 2;  // Gaussian + exponential, one exp per event
 
 // exp for the FCN data pass.  libdevice's: a 64-entry shared-memory table
 // variant (11 FP64 ops instead of ~17) measured slower on B200 (40.6 vs 36.1 us
@@ -57,6 +67,28 @@ __device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
   return c.amp[0] * fcn_exp(-0.5 * z * z) + c.amp[1] * fcn_exp(x * c.scale[1]);
 }
 
+// d = a0 e^A + a1 e^B = e^M (a0 e^(A-M) + a1 e^(B-M)), M = max(A, B): one
+// exp per event (of min - max <= 0) instead of two.  ln d = M + ln s is then
+// summed as sum M + ln(prod s).  Returns false -- the caller falls back to
+// density_ge and its positivity check -- unless M is inside the window where
+// both reference terms are finite and the larger one is a normal positive
+// double, and s is positive and finite: then d > 0 and finite exactly as the
+// reference computes it, and only the rounding differs (a few ulp per event).
+// The host admits this path only for amps in (1e-250, 1e300) with a finite
+// sum, so inside the window t = e^(min-max) is in [0, 1] and s lies in
+// [min amp, amp0 + amp1]: positive and finite, no separate check.  A NaN or
+// infinite x makes M NaN or infinite and fails the window.
+__device__ __forceinline__ bool density_factored(const Coeffs& c, double x, double* s, double* M) {
+  const double z = (x - c.shift[0]) * c.scale[0];
+  const double A = -0.5 * z * z;
+  const double B = x * c.scale[1];
+  const bool ga = A >= B;  // NaN: false, M = B = NaN
+  *M = ga ? A : B;
+  const double t = fcn_exp(ga ? B - A : A - B);
+  *s = ga ? c.amp[0] + c.amp[1] * t : c.amp[0] * t + c.amp[1];
+  return *M > c.m_lo && *M < c.m_hi;
+}
+
 // sum_e ln d_e as ln(prod_e d_e), the product kept as a mantissa in [1, 2^16)
 // and an integer binary exponent: one log per 16 events instead of 16, the
 // exponent bookkeeping on the integer pipe.  Each product step rounds once
@@ -77,6 +109,14 @@ struct LogProd {
     m *= __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
   }
 
+  // move m's binary exponent into e (exact): keeps m in [1, 2) so a thread
+  // can multiply any number of events with one log at the end
+  __device__ __forceinline__ void renorm() {
+    const long long b = __double_as_longlong(m);
+    e += (int)((b >> 52) & 0x7ff) - 1023;
+    m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+  }
+
   __device__ __forceinline__ double value() const {
     const double ln2_hi = 6.93147180369123816490e-01;  // 32 significant bits: e * ln2_hi is exact
     const double ln2_lo = 1.90821492927058770002e-10;
@@ -93,36 +133,45 @@ constexpr int kFcnRows = kFcnTile / kBlock;
 
 // One tile: returns sum ln d over this thread's rows; flags
 // d <= 0 / non-finite (fitting.py:200-205) as ~row in *bad (max = first row).
-template <bool GE>
+template <int V>
+__device__ __forceinline__ void fcn_row(const Coeffs& c, double xv, int64_t row, LogProd& lp,
+                                       double& msum, unsigned long long* bad) {
+  if (V == kFcnFactored) {
+    double s, M;
+    if (density_factored(c, xv, &s, &M)) {
+      lp.add(s);
+      msum += M;
+      return;
+    }
+  }
+  const double d = V == kFcnGeneric ? density(c, xv) : density_ge(c, xv);
+  if (!(d > 0.0) || !isfinite(d)) *bad = max(*bad, ~(unsigned long long)row);
+  lp.add(d);
+}
+
+template <int V>
 __device__ __forceinline__ double chunk_logsum(const double* __restrict__ x, int64_t n,
                                                const Coeffs& c, int64_t ch,
                                                unsigned long long* bad) {
   const int64_t r0 = ch * kFcnTile + threadIdx.x;
   LogProd lp;
+  double msum = 0.0;
   if (ch * kFcnTile + kFcnTile <= n) {
     double xv[kFcnRows];
 #pragma unroll
     for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
 #pragma unroll
-    for (int i = 0; i < kFcnRows; ++i) {
-      const double d = GE ? density_ge(c, xv[i]) : density(c, xv[i]);
-      if (!(d > 0.0) || !isfinite(d)) *bad = max(*bad, ~(unsigned long long)(r0 + i * kBlock));
-      lp.add(d);
-    }
+    for (int i = 0; i < kFcnRows; ++i) fcn_row<V>(c, xv[i], r0 + i * kBlock, lp, msum, bad);
   } else {
     for (int i = 0; i < kFcnRows; ++i) {
       const int64_t r = r0 + i * kBlock;
-      if (r < n) {
-        const double d = GE ? density_ge(c, __ldg(x + r)) : density(c, __ldg(x + r));
-        if (!(d > 0.0) || !isfinite(d)) *bad = max(*bad, ~(unsigned long long)r);
-        lp.add(d);
-      }
+      if (r < n) fcn_row<V>(c, __ldg(x + r), r, lp, msum, bad);
     }
   }
-  return lp.value();
+  return V == kFcnFactored ? lp.value() + msum : lp.value();
 }
 
-template <bool GE>
+template <int V>
 __global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, int64_t n,
                                                 const __grid_constant__ Coeffs c,
                                                 double* __restrict__ part,
@@ -130,7 +179,7 @@ __global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, in
   const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
   for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
     unsigned long long bad = 0;
-    double acc[1] = {chunk_logsum<GE>(x, n, c, ch, &bad)};
+    double acc[1] = {chunk_logsum<V>(x, n, c, ch, &bad)};
     if (bad) record_bad(first_bad, ~bad);
     block_sum_store<1>(acc, part + ch);
   }
@@ -152,26 +201,32 @@ struct FcnWork {
   unsigned long long seq;
 };
 
-template <bool GE>
 // 4 CTAs/SM (64 registers) measured best for the one-launch FCN on B200:
 // C-ABI call 47.8 us; 5 CTAs (48 regs + spills) 50.6, 6 CTAs 53.9, 8 CTAs 64.4,
 // and an unconstrained (256, 1) bound lets ptxas take 216 registers (82 us).
 #ifndef HK_FCN_MIN_BLOCKS
 #define HK_FCN_MIN_BLOCKS 4
 #endif
+// (A persistent one-wave grid -- 592 CTAs over equal contiguous row ranges,
+// one log per thread -- measured slower on B200: 53.7 us per call with 4-row
+// groups, 60.2 us with 16-row groups and spills, against 44.5 us for tiles.)
+
+template <int V>
 __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const double* __restrict__ x, int64_t n,
                                                       const __grid_constant__ Coeffs c, FcnWork w) {
   const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
   for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
     unsigned long long bad = 0;
-    double acc[1] = {chunk_logsum<GE>(x, n, c, ch, &bad)};
+    double acc[1] = {chunk_logsum<V>(x, n, c, ch, &bad)};
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
+  // block_sum_store's writer is thread 0: it alone fences before the ticket
   __shared__ unsigned int s_ticket;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_ticket = atomicAdd(w.ticket, 1u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_ticket = atomicAdd(w.ticket, 1u);
+  }
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
@@ -291,17 +346,31 @@ int make_coeffs(const hk_model_t* m, Coeffs* c) {
       return HK_EUNSUPPORTED;
     }
   }
+  // factored-path window: amp_k e^M in [~1e-300, ~1e304] for both k
+  c->m_lo = 0.0;
+  c->m_hi = -1.0;  // empty: variant kFcnFactored not applicable
+  if (m->n_comp == 2 && c->amp[0] > 1e-250 && c->amp[1] > 1e-250 && c->amp[0] < 1e300 &&
+      c->amp[1] < 1e300) {
+    c->m_lo = -690.0 - std::log(std::fmin(c->amp[0], c->amp[1]));
+    c->m_hi = 700.0 - std::log(c->amp[0] + c->amp[1]);
+  }
   return HK_OK;
+}
+
+int fcn_variant(const Coeffs& c) {
+  const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
+  if (!ge) return kFcnGeneric;
+  return c.m_lo < c.m_hi ? kFcnFactored : kFcnGE;
 }
 
 int launch_nll(const double* d_x, int64_t n, const Coeffs& c, double* part,
                unsigned long long* bad, cudaStream_t st) {
   const unsigned grid = chunk_grid((n + kFcnTile - 1) / kFcnTile);
-  const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
-  if (ge)
-    k_nll<true><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad);
-  else
-    k_nll<false><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad);
+  switch (fcn_variant(c)) {
+    case kFcnFactored: k_nll<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
+    case kFcnGE: k_nll<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
+    default: k_nll<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
+  }
   return check_launch("k_nll");
 }
 
@@ -435,11 +504,11 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   w.host_mail = mb->d;
   w.seq = ++mb->seq;
   const unsigned grid = chunk_grid((n + kFcnTile - 1) / kFcnTile);
-  const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
-  if (ge)
-    k_nll_fused<true><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
-  else
-    k_nll_fused<false><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
+  switch (fcn_variant(c)) {
+    case kFcnFactored: k_nll_fused<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
+    case kFcnGE: k_nll_fused<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
+    default: k_nll_fused<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
+  }
   if (int rc = check_launch("k_nll_fused")) return rc;
   // The last CTA writes the result into mapped host memory and then the
   // sequence number; spin on it (no memcpy, no stream sync on the fast path).

@@ -360,6 +360,46 @@ def test_nll_first_bad_event(cuda, hk, golden):
         hk.nll(_model(hk, 5.0, 0.5, 3.0, 1.0, 1.0), _store(hk, []), ["x0"])
 
 
+def test_nll_extreme_tails_match_reference_semantics(cuda, hk, oracle):
+    """The one-exp factored FCN path hands events whose exponents leave its
+    safe window back to the reference-order density: tiny-but-positive
+    densities still sum like the oracle, underflow to 0 and overflow to inf
+    raise the reference's message at the same event."""
+    rs = np.random.default_rng(3)
+    base = np.concatenate([rs.normal(5.0, 0.5, 40_000), rs.exponential(3.0, 60_000)])
+    pt = (5.0, 0.5, 3.0, 4e4, 6e4)
+    comps = oracle.gauss_exp_components(*pt)
+    # far tail, still positive and normal: exp(-x/tau) ~ e^-690 .. e^-708, below the
+    # factored window (M < -700 here), so these take the reference-order density.
+    # (Deeper tails make exp(-x/tau) subnormal, where the reference itself keeps
+    # only a few significant bits and no evaluation order can agree to 1e-10.)
+    tail = base.copy()
+    tail[[17, 50_000, 99_999, 123]] = [2070.0, 2105.0, 2115.0, 2124.0]
+    got = hk.nll(_model(hk, *pt), _store(hk, tail), ["x0"])
+    assert got == pytest.approx(oracle.nll(tail, comps), rel=1e-10)
+    # both terms underflow to 0 -> not positive, first such event reported
+    under = base.copy()
+    under[[70_000, 30_000]] = [1e6, 5e5]
+    with pytest.raises(ValueError) as exc:
+        oracle.nll(under, comps)
+    with pytest.raises(ValueError) as got_exc:
+        hk.nll(_model(hk, *pt), _store(hk, under), ["x0"])
+    assert str(got_exc.value) == str(exc.value)
+    # a rising exponential (tau < 0) overflows to inf
+    pt2 = (5.0, 0.5, -3.0, 4e4, 6e4)
+    comps2 = oracle.gauss_exp_components(*pt2)
+    over = base.copy()
+    over[[4242]] = [2500.0]
+    with pytest.raises(ValueError) as exc:
+        oracle.nll(over, comps2)
+    with pytest.raises(ValueError) as got_exc:
+        hk.nll(_model(hk, *pt2), _store(hk, over), ["x0"])
+    assert str(got_exc.value) == str(exc.value)
+    # and the regular rising-exponential case sums like the oracle
+    assert hk.nll(_model(hk, *pt2), _store(hk, base), ["x0"]) == pytest.approx(oracle.nll(base, comps2),
+                                                                                 rel=1e-10)
+
+
 def test_nll_data_stays_resident(cuda, hk):
     data = _store(hk, np.linspace(1.0, 9.0, 100_001))
     m = _model(hk, 5.0, 0.5, 3.0, 2e4, 3e4)
