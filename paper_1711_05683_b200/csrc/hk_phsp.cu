@@ -205,8 +205,11 @@ struct ChainArgs {
 };
 
 // daughter mass from its four columns (phasespace.py:259-260) + check (:261-262)
+// sqrt(np.maximum(m2, 0)): the branch-free correctly rounded cr_sqrt over its
+// normal domain (every massive daughter), the IEEE routine otherwise.
 __device__ __forceinline__ double frame_mass(double fe, double fx, double fy, double fz) {
-  return sqrt(max0(fe * fe - fx * fx - fy * fy - fz * fz));
+  const double m2 = fe * fe - fx * fx - fy * fy - fz * fz;
+  return m2 > 1e-300 && m2 < 1e300 ? cr_sqrt(m2) : sqrt(max0(m2));
 }
 
 __device__ __forceinline__ bool mass_mismatch(double fm, double M) {
@@ -256,17 +259,17 @@ struct GenChainArgs {
 // Compile-time recursion over J keeps p[] in registers (a runtime-trip loop
 // with a skip made nvcc demote p[] to local memory).
 template <int J, int N, int NS>
-__device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a,
+__device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a, int k,
                                                        const double (&p)[4 * N], int64_t r) {
   if constexpr (J < N) {
-    if (J != a.k) {
-      const int slot = 1 + 4 * (J < a.k ? J : J + NS - 1);
+    if (J != k) {
+      const int slot = 1 + 4 * (J < k ? J : J + NS - 1);
       __stcs(a.cols[slot + 0] + r, p[4 * J + 0]);
       __stcs(a.cols[slot + 1] + r, p[4 * J + 1]);
       __stcs(a.cols[slot + 2] + r, p[4 * J + 2]);
       __stcs(a.cols[slot + 3] + r, p[4 * J + 3]);
     }
-    store_parent_daughters<J + 1, N, NS>(a, p, r);
+    store_parent_daughters<J + 1, N, NS>(a, k, p, r);
   }
 }
 
@@ -276,9 +279,12 @@ __device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a,
 // One fused chain event (generation, decay of daughter k, splice-ordered
 // stores); returns the event weight.  Branch-free apart from the moving-mother
 // test so two calls interleave; a mass mismatch lowers *bad to the row.
-template <int N, int NS, int MODE>
+// K >= 0: the decaying daughter as a compile-time index (the hot 3-body
+// parent), so its four-vector is a register reference instead of a select chain.
+template <int N, int NS, int MODE, int K>
 __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, int64_t r,
                                             unsigned long long* bad) {
+  const int k = K >= 0 ? K : a.k;
   const uint64_t row = a.ev_begin + (uint64_t)r;
   double p[4 * N];
   const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
@@ -289,13 +295,20 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
   // daughter k's four-momentum; selp in asm so the front end cannot turn the
   // select chain back into p[4k] (which demotes p[] to local memory)
   double fe = 0.0, fx = 0.0, fy = 0.0, fz = 0.0;
+  if constexpr (K >= 0) {
+    fe = p[4 * K];
+    fx = p[4 * K + 1];
+    fy = p[4 * K + 2];
+    fz = p[4 * K + 3];
+  } else {
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const bool sel = j == a.k;
-    fe = select_f64(sel, p[4 * j], fe);
-    fx = select_f64(sel, p[4 * j + 1], fx);
-    fy = select_f64(sel, p[4 * j + 2], fy);
-    fz = select_f64(sel, p[4 * j + 3], fz);
+    for (int j = 0; j < N; ++j) {
+      const bool sel = j == k;
+      fe = select_f64(sel, p[4 * j], fe);
+      fx = select_f64(sel, p[4 * j + 1], fx);
+      fy = select_f64(sel, p[4 * j + 2], fy);
+      fz = select_f64(sel, p[4 * j + 3], fz);
+    }
   }
   const double fm = frame_mass(fe, fx, fy, fz);
   *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
@@ -306,14 +319,14 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
   for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
   const double w = wp * ws;
   __stcs(a.cols[0] + r, w);
-  store_parent_daughters<0, N, NS>(a, p, r);
-  const int sbase = 1 + 4 * a.k;
+  store_parent_daughters<0, N, NS>(a, k, p, r);
+  const int sbase = 1 + 4 * k;
 #pragma unroll
   for (int j = 0; j < 4 * NS; ++j) __stcs(a.cols[sbase + j] + r, q[j]);
   return w;
 }
 
-template <int N, int NS, int MODE>
+template <int N, int NS, int MODE, int K>
 __global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_constant__ GenChainArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
@@ -326,8 +339,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_const
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
         const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
-        const double w0 = chain_row<N, NS, MODE>(a, mf, r0, &bad);
-        const double w1 = chain_row<N, NS, MODE>(a, mf, r0 + HK_CHUNK / 2, &bad);
+        const double w0 = chain_row<N, NS, MODE, K>(a, mf, r0, &bad);
+        const double w1 = chain_row<N, NS, MODE, K>(a, mf, r0 + HK_CHUNK / 2, &bad);
         acc[0] += w0;
         acc[1] += w0 * w0;
         acc[0] += w1;
@@ -338,7 +351,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_const
       for (int i = 0; i < kRowsPerThread; ++i) {
         const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
         if (r < a.count) {
-          const double w = chain_row<N, NS, MODE>(a, mf, r, &bad);
+          const double w = chain_row<N, NS, MODE, K>(a, mf, r, &bad);
           acc[0] += w;
           acc[1] += w * w;
         }
@@ -588,12 +601,19 @@ int dispatch_chain(const ChainArgs& a, unsigned grid, cudaStream_t st) {
   return check_launch("k_chain");
 }
 
+// (A compile-time decaying-daughter index for 3-body parents -- no select
+// chain -- measured no faster on B200: 4.63 vs 4.56 ms per 1.25e8 C3 events.)
+template <int N, int NS, int MODE>
+void launch_gen_chain(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
+  k_generate_chain<N, NS, MODE, -1><<<grid, kBlock, 0, st>>>(a);
+}
+
 template <int MODE, int N>
 int dispatch_gen_chain_sub(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
   switch (a.sub.n) {
-    case 2: k_generate_chain<N, 2, MODE><<<grid, kBlock, 0, st>>>(a); break;
-    case 3: k_generate_chain<N, 3, MODE><<<grid, kBlock, 0, st>>>(a); break;
-    case 4: k_generate_chain<N, 4, MODE><<<grid, kBlock, 0, st>>>(a); break;
+    case 2: launch_gen_chain<N, 2, MODE>(a, grid, st); break;
+    case 3: launch_gen_chain<N, 3, MODE>(a, grid, st); break;
+    case 4: launch_gen_chain<N, 4, MODE>(a, grid, st); break;
     default:
       set_error("fused chain supports 2..4 sub-daughters, got %d", a.sub.n);
       return HK_EUNSUPPORTED;
