@@ -110,3 +110,55 @@ def sharded_integrate(expr, spec, mother, n_total: int, key, arg_builder, group=
     full = gather_partials(parts, n_total, 5, group)
     tot = _lib.fold(full, (n_total + CHUNK - 1) // CHUNK, 5)
     return _finish_average(tot.cpu().numpy(), n_total)
+
+
+def shard_rows(store, rank: int, world: int):
+    """The rank's contiguous row range of a store, as a zero-copy device view
+    (the C4 layout: the data set split by row range once, resident per GPU)."""
+    from .store import ColumnStore  # noqa: PLC0415
+    a, b = shard_range(len(store), rank, world)
+    cols = [store.device_column(name)[a:b] for name in store.schema.names]
+    return ColumnStore._from_device(store.schema, cols), a
+
+
+def combine_nll_parts(parts, expected_total: float) -> float:
+    """Fold per-rank (event log-sum, global first-bad row or -1, its density)
+    triples in rank order: deterministic for a fixed GPU count.  The smallest
+    bad row wins, as in the reference (fitting.py:200-205)."""
+    import numpy as np  # noqa: PLC0415
+    bad = [(int(row), val) for _, row, val in parts if row >= 0]
+    if bad:
+        row, val = min(bad)
+        raise ValueError(f"model density {np.float64(val)!r} is not positive at event {row}")
+    total = 0.0
+    for logsum, _, _ in parts:
+        total += logsum
+    return expected_total - total
+
+
+def sharded_nll(model, shard, observable_columns, row_offset: int, group=None) -> float:
+    """nll (fitting.py:175-210) over a data set split by row range across the
+    process group: each rank runs the fused FCN pass over its resident rows,
+    then one all-gather of 3 doubles per rank and the same rank-order fold on
+    every rank, so all ranks return the same value (a minimiser can run in
+    lock-step on every rank).  `row_offset` is the shard's first global row,
+    so a bad event is reported by its global index."""
+    from .fitting import nll_event_sum  # noqa: PLC0415
+    rank, world = dist_info(group)
+    if len(shard):
+        logsum, first, val = nll_event_sum(model, shard, observable_columns)
+    else:
+        logsum, first, val = 0.0, None, None
+    if world == 1:
+        if first is not None:
+            raise ValueError(f"model density {val!r} is not positive at event {row_offset + first}")
+        return model.expected_total() - logsum
+    mine = (logsum, -1.0 if first is None else float(row_offset + first), 0.0 if val is None else float(val))
+    torch = _lib.torch()
+    dist = torch.distributed
+    dev = _lib.device() if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(mine, dtype=torch.float64, device=dev)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    parts = torch.stack(out).cpu().tolist()
+    return combine_nll_parts([tuple(p) for p in parts], model.expected_total())

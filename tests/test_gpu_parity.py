@@ -400,6 +400,42 @@ def test_nll_extreme_tails_match_reference_semantics(cuda, hk, oracle):
                                                                                  rel=1e-10)
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_sharded_nll(cuda, hk, oracle, world):
+    """C4 at N GPUs, emulated on one: per-shard fused passes over zero-copy row
+    views, folded in rank order (parallel.combine_nll_parts), equal the
+    one-pass nll and the oracle; a bad event keeps its global index."""
+    from paper_1711_05683_b200 import parallel
+    from paper_1711_05683_b200.fitting import nll_event_sum
+    rs = np.random.default_rng(11)
+    x = np.concatenate([rs.normal(5.0, 0.5, 400_000), rs.exponential(3.0, 600_000)])
+    x = x[(x > 0) & (x < 10)]
+    pt = (4.9, 0.55, 2.8, 4e5, 6e5)
+    model = _model(hk, *pt)
+    data = _store(hk, x)
+
+    def sharded(store):
+        parts = []
+        for r in range(world):
+            shard, a = parallel.shard_rows(store, r, world)
+            logsum, first, val = nll_event_sum(model, shard, ["x0"])
+            parts.append((logsum, -1.0 if first is None else float(a + first),
+                          0.0 if val is None else float(val)))
+        return parallel.combine_nll_parts(parts, model.expected_total())
+
+    got = sharded(data)
+    assert got == pytest.approx(hk.nll(model, data, ["x0"]), rel=1e-12)
+    assert got == pytest.approx(oracle.nll(x, oracle.gauss_exp_components(*pt)), rel=1e-10)
+    assert parallel.sharded_nll(model, data, ["x0"], 0) == hk.nll(model, data, ["x0"])  # world 1
+    bad = x.copy()
+    bad[[len(x) - 5, len(x) // 2 + 3]] = np.nan
+    with pytest.raises(ValueError) as want:
+        hk.nll(model, _store(hk, bad), ["x0"])
+    with pytest.raises(ValueError) as exc:
+        sharded(_store(hk, bad))
+    assert str(exc.value) == str(want.value)
+
+
 def test_nll_data_stays_resident(cuda, hk):
     data = _store(hk, np.linspace(1.0, 9.0, 100_001))
     m = _model(hk, 5.0, 0.5, 3.0, 2e4, 3e4)
