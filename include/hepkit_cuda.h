@@ -316,6 +316,17 @@ int hk_compact(const double* const* d_in, int32_t n_cols, int64_t n, const uint8
 int hk_scan_counts(const int64_t* d_counts, int64_t n, int64_t* d_out, int64_t* d_total,
                    void* stream);
 
+/* ------------------------------------------------------------------- CSV */
+/* The body of ColumnStore.write_csv (store.py:181-204) for real64 columns:
+ * rows [0, n_rows) of the n_cols device columns as text, each value exactly
+ * Python's f"{v:.17g}" (correctly rounded 17 significant digits; nan, inf,
+ * -inf, -0), ',' between columns, '\n' after every row -- no header.
+ * d_scratch: hk_csv_scratch_bytes(n_rows, n_cols) bytes; d_out: at least
+ * n_rows * n_cols * 25 bytes.  Synchronous: *h_len = bytes of text written. */
+int64_t hk_csv_scratch_bytes(int64_t n_rows, int32_t n_cols);
+int hk_format_csv(const double* const* d_cols, int32_t n_cols, int64_t n_rows, void* d_scratch,
+                  char* d_out, int64_t out_cap, int64_t* h_len, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,13 @@ def test_every_entry_point_marshals_and_validates(hk):
     assert L.hk_compact(cols, 13, 0, dp, dp, cols, 0, None) == OK
     lo = (ctypes.c_double * 1)(0.0)
     assert L.hk_sample_pdf(prog, 1, lo, lo, 1.0, k, 0, 0, 10, cols, dp, None) == OK
+    assert L.hk_csv_scratch_bytes(0, 13) == 0
+    assert L.hk_csv_scratch_bytes(1000, 13) > 1000 * 13 * 24
+    text_len = ctypes.c_int64(-1)
+    assert L.hk_format_csv(cols, 13, 0, None, None, 0, ctypes.byref(text_len), None) == OK
+    assert text_len.value == 0
+    assert L.hk_format_csv(cols, 13, 10, dp, dp, 100, ctypes.byref(text_len), None) == _lib.HK_EINVAL
+    assert "capacity" in _lib.last_error()
     # validation errors come back as HK_EINVAL with a message
     assert L.hk_nll_eval(dp, 0, model, dp, two, ctypes.byref(ctypes.c_uint64()), None) == _lib.HK_EINVAL
     assert "empty" in _lib.last_error()
