@@ -234,6 +234,13 @@ def ptr_array(tensors) -> ctypes.Array:
     return arr
 
 
+def ptr_rows(block) -> ctypes.Array:
+    """Column pointers of a 2-D (columns x stride) fp64 block, without
+    materialising per-column tensors."""
+    base, step = block.data_ptr(), block.stride(0) * block.element_size()
+    return (ctypes.c_void_p * block.shape[0])(*[base + i * step for i in range(block.shape[0])])
+
+
 def empty(n: int, dtype=None):
     t = torch()
     return t.empty(int(n), dtype=dtype or t.float64, device=device())

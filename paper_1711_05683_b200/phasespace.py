@@ -21,6 +21,7 @@ on any GPU is bit-identical to rows a..b of a one-shot run.
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 from dataclasses import dataclass
 
@@ -60,6 +61,7 @@ class DecaySpec:
         return len(self.daughter_masses)
 
 
+@functools.lru_cache(maxsize=64)
 def phsp_schema(n_daughters: int) -> ColumnSchema:
     """weight, p1_e, p1_px, p1_py, p1_pz, ... (phasespace.py:60-64)."""
     names = ["weight"]
@@ -75,8 +77,24 @@ def _check_mother(spec: DecaySpec, mother: FourVector) -> float:
     return m
 
 
+def _column_block(n_cols: int, n: int, extra: int = 0):
+    """n_cols device columns of n fp64 values carved out of ONE allocation
+    (each column 256-byte aligned, so warp stores stay whole transactions),
+    plus an `extra`-double tail for partials: one caching-allocator call
+    instead of n_cols + 1 -- the host cost of small (C1-size) calls."""
+    stride = (n + 31) // 32 * 32
+    buf = _lib.empty(n_cols * stride + extra)
+    return buf[: n_cols * stride].view(n_cols, stride), buf[n_cols * stride:]
+
+
 def _columns(n_cols: int, n: int) -> list:
-    return [_lib.empty(n) for _ in range(n_cols)]
+    return list(_column_block(n_cols, n)[0][:, :n].unbind(0))
+
+
+@functools.lru_cache(maxsize=256)
+def _decay_struct(spec: DecaySpec, mother: tuple, m_mother: float):
+    """hk_decay_t per (spec, mother): read-only to the library, so shared."""
+    return _lib.make_decay(spec, FourVector(*mother), m_mother)
 
 
 def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKey,
@@ -95,14 +113,13 @@ def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKe
     n_events = int(n_events)
     if n_events < 0:
         raise ValueError(f"n_events must be >= 0, got {n_events}")
-    d = _lib.make_decay(spec, mother, m_mother)
+    d = _decay_struct(spec, (mother.e, mother.px, mother.py, mother.pz), m_mother)
     k = _lib.make_key(key, rng_mode(rng))
-    cols = _columns(4 * spec.n + 1, n_events)
-    store = ColumnStore._from_device(phsp_schema(spec.n), cols)
+    block, wpart = _column_block(4 * spec.n + 1, n_events, 2 * _lib.num_weight_slices(n_events))
+    store = ColumnStore._from_block(phsp_schema(spec.n), block, n_events)
     if n_events == 0:
         return store
-    wpart = _lib.empty(2 * _lib.num_weight_slices(n_events))
-    _lib.check(_lib.lib().hk_phsp_generate(d, k, _lib.u64(row_offset), n_events, _lib.ptr_array(cols),
+    _lib.check(_lib.lib().hk_phsp_generate(d, k, _lib.u64(row_offset), n_events, _lib.ptr_rows(block),
                                            _lib.ptr(wpart), _lib.stream_ptr()), "hk_phsp_generate")
     store.meta["weight_partials"] = wpart
     return store
