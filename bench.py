@@ -280,7 +280,7 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
     ev1.synchronize()
     kt = max_over_ranks(ev0.elapsed_time(ev1) / evals * 1e-3)
     # the one-launch C-ABI FCN call alone (kernel + mapped-memory result), no Python
-    work = torch.zeros(_lib.num_fcn_tiles(n_local) + 4, dtype=torch.float64, device=x.device)
+    work = torch.zeros(int(_lib.lib().hk_nll_work_doubles(n_local)), dtype=torch.float64, device=x.device)
     logsum, first = ctypes.c_double(), ctypes.c_uint64()
     for _ in range(3):
         _lib.lib().hk_nll_eval(_lib.ptr(x), n_local, lm, _lib.ptr(work), ctypes.byref(logsum),

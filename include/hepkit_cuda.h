@@ -262,10 +262,14 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
  * *h_first_bad = first failing row or HK_NO_BAD_ROW.  One kernel launch (the
  * last CTA folds the tile partials in a fixed order and publishes the result
  * into mapped pinned host memory, which the caller's thread polls).  d_work
- * needs ceil(n / HK_FCN_TILE) + 4 doubles, ZERO-FILLED before its first use;
- * the kernel re-arms it for the next call. */
+ * needs hk_nll_work_doubles(n) doubles, ZERO-FILLED before its first use;
+ * the kernel re-arms it for the next call.  Rows are scheduled as whole
+ * waves of HK_FCN_TILE-row tiles plus the leftover spread over one wave, so
+ * the sum's grouping (not its value beyond rounding) depends on the SM count. */
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
+/* workspace size of hk_nll_eval for n rows (4 + one partial per scheduled CTA) */
+int64_t hk_nll_work_doubles(int64_t n);
 
 /* Yield-stationarity sums (fitting.py:401-434) and the sWeights matrix
  * accumulation (splot.py:45-87) for K <= 4 components: per chunk K values

@@ -41,7 +41,7 @@ EXPORTS = (
     "hk_yield_partials", "hk_splot_weights",
     "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
     "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
-    "hk_csv_scratch_bytes", "hk_format_csv",
+    "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles",
 )
 
 
@@ -131,6 +131,7 @@ _SIGS = {
     "hk_jit_source": (_I64, [_F, _I32, _I32, ctypes.c_char_p, _I64]),
     "hk_jit_compile": (_INT, [_F, _I32, _I32, ctypes.POINTER(_I64)]),
     "hk_csv_scratch_bytes": (_I64, [_I64, _I32]),
+    "hk_nll_work_doubles": (_I64, [_I64]),
     "hk_format_csv": (_INT, [_PP, _I32, _I64, _P, _P, _I64, ctypes.POINTER(_I64), _P]),
 }
 

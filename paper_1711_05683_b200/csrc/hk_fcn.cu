@@ -149,26 +149,45 @@ __device__ __forceinline__ void fcn_row(const Coeffs& c, double xv, int64_t row,
   lp.add(d);
 }
 
+// sum ln d over rows [begin, end) (at most one tile): all 16 loads in flight
+// for a full tile, a guarded loop otherwise
 template <int V>
-__device__ __forceinline__ double chunk_logsum(const double* __restrict__ x, int64_t n,
-                                               const Coeffs& c, int64_t ch,
+__device__ __forceinline__ double range_logsum(const double* __restrict__ x, int64_t begin,
+                                               int64_t end, const Coeffs& c,
                                                unsigned long long* bad) {
-  const int64_t r0 = ch * kFcnTile + threadIdx.x;
+  const int64_t r0 = begin + threadIdx.x;
   LogProd lp;
   double msum = 0.0;
-  if (ch * kFcnTile + kFcnTile <= n) {
+  if (end - begin == kFcnTile) {
     double xv[kFcnRows];
 #pragma unroll
     for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
 #pragma unroll
     for (int i = 0; i < kFcnRows; ++i) fcn_row<V>(c, xv[i], r0 + i * kBlock, lp, msum, bad);
-  } else {
-    for (int i = 0; i < kFcnRows; ++i) {
-      const int64_t r = r0 + i * kBlock;
-      if (r < n) fcn_row<V>(c, __ldg(x + r), r, lp, msum, bad);
+  } else {  // short range: groups of 4 loads in flight, stop at the CTA's last row
+    for (int i0 = 0; i0 < kFcnRows && begin + i0 * kBlock < end; i0 += 4) {
+      double xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t r = r0 + (i0 + k) * kBlock;
+        xv[k] = r < end ? __ldg(x + r) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t r = r0 + (i0 + k) * kBlock;
+        if (r < end) fcn_row<V>(c, xv[k], r, lp, msum, bad);
+      }
     }
   }
   return V == kFcnFactored ? lp.value() + msum : lp.value();
+}
+
+template <int V>
+__device__ __forceinline__ double chunk_logsum(const double* __restrict__ x, int64_t n,
+                                               const Coeffs& c, int64_t ch,
+                                               unsigned long long* bad) {
+  const int64_t b = ch * kFcnTile;
+  return range_logsum<V>(x, b, b + kFcnTile < n ? b + kFcnTile : n, c, bad);
 }
 
 template <int V>
@@ -199,7 +218,23 @@ struct FcnWork {
   // host_mail[1..2] = out[0..1], then host_mail[0] = seq (after a system fence)
   volatile unsigned long long* host_mail;
   unsigned long long seq;
+  // tile schedule (fcn_schedule): CTA b < full owns tile b (4096 rows); the
+  // rows from full * 4096 on are split evenly over tail_ctas more CTAs, so
+  // the last wave is short instead of a few full tiles on an idle GPU
+  int64_t full, tail_ctas;
 };
+
+__device__ __forceinline__ void fcn_range(const FcnWork& w, int64_t n, int64_t b, int64_t* begin,
+                                          int64_t* end) {
+  if (b < w.full) {
+    *begin = b * kFcnTile;
+    *end = *begin + kFcnTile;
+    return;
+  }
+  const int64_t t0 = w.full * kFcnTile, rem = n - t0, j = b - w.full;
+  *begin = t0 + rem * j / w.tail_ctas;
+  *end = t0 + rem * (j + 1) / w.tail_ctas;
+}
 
 // 4 CTAs/SM (64 registers) measured best for the one-launch FCN on B200:
 // C-ABI call 47.8 us; 5 CTAs (48 regs + spills) 50.6, 6 CTAs 53.9, 8 CTAs 64.4,
@@ -214,10 +249,12 @@ struct FcnWork {
 template <int V>
 __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const double* __restrict__ x, int64_t n,
                                                       const __grid_constant__ Coeffs c, FcnWork w) {
-  const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
+  const int64_t chunks = w.full + w.tail_ctas;
   for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
     unsigned long long bad = 0;
-    double acc[1] = {chunk_logsum<V>(x, n, c, ch, &bad)};
+    int64_t begin, end;
+    fcn_range(w, n, ch, &begin, &end);
+    double acc[1] = {range_logsum<V>(x, begin, end, c, &bad)};
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
@@ -468,11 +505,46 @@ int mailbox(Mailbox** out) {
   return HK_OK;
 }
 
+// Tile schedule of the one-launch FCN: plain 4096-row tiles.  The spread-tail
+// variant (kFcnSpreadTail: whole waves of S = SMs x 4 tiles, then the leftover
+// rows split over one wave of short CTAs, 4 x 592 + 592 CTAs for 1e7 events
+// instead of 2442 tiles) measured slower on B200 -- C-ABI call 44.6 vs 40.8 us:
+// a wave of short CTAs costs about the same latency as the 74-tile tail it
+// replaces.  Kept behind the switch for the record.
+constexpr bool kFcnSpreadTail = false;
+
+void fcn_schedule(int64_t n, int64_t* full, int64_t* tail_ctas) {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = (sms > 0 ? sms : 148) * HK_FCN_MIN_BLOCKS;
+  }
+  const int64_t tiles = (n + kFcnTile - 1) / kFcnTile;
+  if (!kFcnSpreadTail || tiles <= slots) {  // plain tiles
+    *full = n / kFcnTile;
+    *tail_ctas = n % kFcnTile ? 1 : 0;
+    return;
+  }
+  *full = (n / kFcnTile / slots) * slots;  // whole waves of whole tiles
+  const int64_t rem = n - *full * kFcnTile;
+  const int64_t want = (rem + kBlock - 1) / kBlock;
+  *tail_ctas = rem == 0 ? 0 : (want < slots ? want : slots);
+}
+
 }  // namespace hk
 
 using namespace hk;
 
 extern "C" {
+
+int64_t hk_nll_work_doubles(int64_t n) {
+  if (n <= 0) return 4;
+  int64_t full, tail;
+  fcn_schedule(n, &full, &tail);
+  return 4 + full + tail;
+}
 
 int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                     uint64_t* d_first_bad, void* stream) {
@@ -503,7 +575,8 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   if (int rc = mailbox(&mb)) return rc;
   w.host_mail = mb->d;
   w.seq = ++mb->seq;
-  const unsigned grid = chunk_grid((n + kFcnTile - 1) / kFcnTile);
+  fcn_schedule(n, &w.full, &w.tail_ctas);
+  const unsigned grid = chunk_grid(w.full + w.tail_ctas);
   switch (fcn_variant(c)) {
     case kFcnFactored: k_nll_fused<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     case kFcnGE: k_nll_fused<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;

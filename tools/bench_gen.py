@@ -68,7 +68,7 @@ def main():
     # one-launch FCN through the C ABI (k_nll_fused + mailbox), synchronous per call
     import ctypes
     import time
-    work = torch.zeros(_lib.num_fcn_tiles(x.numel()) + 4, dtype=torch.float64, device="cuda")
+    work = torch.zeros(int(_lib.lib().hk_nll_work_doubles(x.numel())), dtype=torch.float64, device="cuda")
     ls, fb = ctypes.c_double(), ctypes.c_uint64()
     for _ in range(20):
         L.hk_nll_eval(_lib.ptr(x), x.numel(), lm, _lib.ptr(work), ctypes.byref(ls), ctypes.byref(fb), st.cuda_stream)
