@@ -259,11 +259,7 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
     dt = ev0.elapsed_time(ev1) * 1e-3 / evals
 
     def max_over_ranks(v: float) -> float:
-        if not dist:
-            return v
-        t = torch.tensor([v], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(torch, dist, v)
 
     dt = max_over_ranks(dt)
     # device-only time of the FCN pass over this rank's rows
@@ -313,12 +309,17 @@ def _timed(torch, fn, reps: int, dist=None) -> float:
         fn()
     e1.record(st)
     e1.synchronize()
-    dt = e0.elapsed_time(e1) * 1e-3 / reps
-    if dist:
-        t = torch.tensor([dt], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    return dt
+    return _max_over_ranks(torch, dist, e0.elapsed_time(e1) * 1e-3 / reps)
+
+
+def _max_over_ranks(torch, dist, v: float) -> float:
+    """Max of a per-rank time over the process group (NCCL on device tensors;
+    a CPU tensor under the gloo test backend)."""
+    if not dist:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
@@ -442,11 +443,19 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HK_BENCH_BACKEND=gloo + HK_BENCH_DEVICE=0: exercise the N>1 code path with
+    # several ranks on one GPU (independent kernels, CPU collectives) -- a
+    # correctness check of the multi-rank plumbing, never a bench number
+    local = int(os.environ.get("HK_BENCH_DEVICE", local))
+    backend = os.environ.get("HK_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
     n = EVENTS_PER_GPU
     n_total = n * world
@@ -486,10 +495,7 @@ def run_ours(args) -> None:
         dist.barrier()
     elapsed = t0.elapsed_time(t1) * 1e-3
     gen_times = [a.elapsed_time(b) * 1e-3 for a, b in gen_ev]
-    if dist:
-        tt = torch.tensor([elapsed], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
+    elapsed = _max_over_ranks(torch, dist, elapsed)
     sums = tot.cpu().numpy()
     per_step = elapsed / args.steps
     value = n_total / per_step
@@ -517,9 +523,7 @@ def run_ours(args) -> None:
                "api": "phsp_generate_to_host (pinned host columns; generation overlapped with D2H)",
                "steps": e_steps}
         if dist:
-            tt = torch.tensor([e_dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = n_total / float(tt.item())
+            e2e["value"] = n_total / _max_over_ranks(torch, dist, e_dt)
         del host
 
     others = None if args.no_configs else other_configs(hk, torch, _lib, rank, world, dist)

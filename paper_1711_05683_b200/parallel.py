@@ -80,11 +80,13 @@ def gather_partials(local, n_total: int, width: int, group=None):
     nch = (n_total + CHUNK - 1) // CHUNK
     sizes = [(nch * (r + 1) // world - nch * r // world) for r in range(world)]
     cap = max(sizes) * width
-    buf = torch.zeros(cap, dtype=local.dtype, device=local.device)
-    buf[: local.numel()] = local
+    # NCCL gathers device tensors in place; CPU backends (gloo) go through host memory
+    dev = local.device if dist.get_backend(group) == "nccl" else "cpu"
+    buf = torch.zeros(cap, dtype=local.dtype, device=dev)
+    buf[: local.numel()] = local.to(dev)
     out = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(out, buf, group=group)
-    return torch.cat([o[: s * width] for o, s in zip(out, sizes)])
+    return torch.cat([o[: s * width] for o, s in zip(out, sizes)]).to(local.device)
 
 
 def sharded_weight_moments(block_shard, n_total: int, group=None):
