@@ -326,8 +326,16 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
   return w;
 }
 
+// chain kernel shape: events per thread iteration (ILP) and CTAs per SM
+#ifndef HK_CHAIN_ILP
+#define HK_CHAIN_ILP 2
+#endif
+#ifndef HK_CHAIN_MINB
+#define HK_CHAIN_MINB 2
+#endif
+
 template <int N, int NS, int MODE, int K>
-__global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_constant__ GenChainArgs a) {
+__global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const __grid_constant__ GenChainArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_generate_chain(const __grid_const
   unsigned long long bad = ~0ull;
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
-    if (N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
+    if (HK_CHAIN_ILP == 2 && N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
         const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;

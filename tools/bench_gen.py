@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--rng", default="reference")
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--chain", action="store_true", help="also time the fused C3 chain")
     a = ap.parse_args()
     n = int(a.n)
     M, ms = 5.27966, (3.0969, 0.493677, 0.13957039)
@@ -44,6 +45,31 @@ def main():
     ms_ = e0.elapsed_time(e1) / a.reps
     out = {"lib": os.environ.get("HK_LIB_PATH", "default"), "n": n, "ms": ms_, "ev_per_s": n / ms_ * 1e3,
            "GBps": 104 * n / ms_ / 1e6}
+    # fused chain (C3): B0 -> J/psi(-> mu mu) K pi, 1.25e8 events, 17 columns
+    if a.chain:
+        gen_check = [c[:200_000].clone() for c in cols] if a.check else None
+        del cols
+        torch.cuda.empty_cache()
+        nc = 125_000_000
+        ccols = [_lib.empty(nc) for _ in range(17)]
+        ccp = _lib.ptr_array(ccols)
+        cw = _lib.empty(2 * _lib.num_weight_slices(nc))
+        cbad = _lib.bad_cells(1)
+        sub = _lib.make_decay(hk.DecaySpec(3.0969, (0.1056583755, 0.1056583755)))
+        sk = _lib.make_key(hk.RngKey(2, 1), hk.rng.rng_mode(a.rng))
+        for _ in range(2):
+            _lib.check(L.hk_phsp_generate_chain(d, k, 1, sub, sk, 0, nc, ccp, _lib.ptr(cw), _lib.ptr(cbad),
+                                                st.cuda_stream), "chain")
+        e0.record()
+        for _ in range(5):
+            L.hk_phsp_generate_chain(d, k, 1, sub, sk, 0, nc, ccp, _lib.ptr(cw), _lib.ptr(cbad), st.cuda_stream)
+        e1.record()
+        e1.synchronize()
+        cms = e0.elapsed_time(e1) / 5
+        out.update({"chain_ms": cms, "chain_ev_per_s": nc / cms * 1e3, "chain_GBps": 136 * nc / cms / 1e6})
+        del ccols
+        torch.cuda.empty_cache()
+        cols = gen_check
     # FCN kernel on 1e7 gauss+exp events (hk_nll_partials, one launch per eval)
     rs = np.random.default_rng(7)
     xs = np.clip(np.concatenate([rs.normal(5.0, 0.5, 4_000_000), rs.exponential(3.0, 6_000_000)]), 1e-3, 9.999)
