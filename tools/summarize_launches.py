@@ -14,7 +14,7 @@ for r in rows[1:]:
     if r[mi] != "gpu__time_duration.sum":
         continue
     v = float(r[vi].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[unit_i], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[r[unit_i]]
     tot[r[ki]] += v * scale
     cnt[r[ki]] += 1
 allt = sum(tot.values())
