@@ -237,6 +237,31 @@ def test_fit_recovers_truth_and_yield_sum(cuda, hk):
         assert abs((ps[name].value - truth[name]) / res.errors[name]) < 5
 
 
+def test_pull_calibration_200_toys(cuda, hk):
+    """test_acceptance.py criterion 3 (pull calibration): 200 toys of ~1e4
+    events, each sampled on the GPU and fitted with the GPU FCN; pulls of all
+    five parameters have |mean| < 0.15 and width in [0.85, 1.15], at most 2
+    failed fits."""
+    truth = {"mean": 5.0, "sigma": 0.5, "tau": 3.0, "n_sig": 4000.0, "n_bkg": 6000.0}
+    pulls = {name: [] for name in truth}
+    failed = 0
+    for t in range(200):
+        model = _toy(hk, scale=0.2)
+        sample = hk.generate_model_sample(model, hk.RngKey(6, 2, counter=t << 40))
+        res = hk.fit(model, sample, ["x0"])
+        if res.status is not hk.FitStatus.CONVERGED:
+            failed += 1
+            continue
+        ps = model.param_set()
+        for name in pulls:
+            pulls[name].append((ps[name].value - truth[name]) / res.errors[name])
+    assert failed <= 2
+    for name, vals in pulls.items():
+        arr = np.asarray(vals)
+        assert abs(float(np.mean(arr))) < 0.15, (name, float(np.mean(arr)))
+        assert 0.85 <= float(np.std(arr, ddof=1)) <= 1.15, (name, float(np.std(arr, ddof=1)))
+
+
 def test_fit_with_everything_fixed(cuda, hk):
     model = _toy(hk, scale=0.01)
     data = hk.generate_model_sample(model, hk.RngKey(62, 2))
