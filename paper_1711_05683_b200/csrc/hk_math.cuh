@@ -106,6 +106,41 @@ HK_HD void sincospi(double t, double* s, double* c) {
   *c = cs;
 }
 
+// sin(pi t), cos(pi t) for the generator's angles (t = 2u in [0, 2), any
+// finite t works): the quadrant reduction above with near-minimax polynomials
+// of degree 13 (sin) and 14 (cos) on |r| <= 1/4 -- max abs error 1.1e-16 in
+// double, like the longer Taylor forms (fitted by tools/fit_sincospi.py).
+// 15 FMA-class ops + the reduction: about 30 instructions where libdevice's
+// sincospi takes 53 on sm_100a (ncu source view of k_generate).
+HK_HD void sincospi_gen(double t, double* s, double* c) {
+  const double q = rint(2.0 * t);
+  const double r = fma(-0.5, q, t);
+  const double r2 = r * r;
+  double ps = 0x1.e3988d39fa62ep-12;
+  ps = fma(ps, r2, -0x1.e2ff4a0c92053p-8);
+  ps = fma(ps, r2, 0x1.50782e688341bp-4);
+  ps = fma(ps, r2, -0x1.32d2cce12a338p-1);
+  ps = fma(ps, r2, 0x1.466bc677567a1p+1);
+  ps = fma(ps, r2, -0x1.4abbce625be21p+2);
+  ps = fma(ps, r2, 0x1.921fb54442d18p+1);
+  double pc = -0x1.b264e50804144p-14;
+  pc = fma(pc, r2, 0x1.f9cc41b007973p-10);
+  pc = fma(pc, r2, -0x1.a6d1ec79e7ce5p-6);
+  pc = fma(pc, r2, 0x1.e1f506835728ep-3);
+  pc = fma(pc, r2, -0x1.55d3c7e3c9108p+0);
+  pc = fma(pc, r2, 0x1.03c1f081b5aacp+2);
+  pc = fma(pc, r2, -0x1.3bd3cc9be45dep+2);
+  pc = fma(pc, r2, 1.0);
+  const double sr = r * ps;
+  const int iq = (int)q;
+  double sn = (iq & 1) ? pc : sr;
+  double cs = (iq & 1) ? sr : pc;
+  sn = (iq & 2) ? -sn : sn;
+  cs = ((iq + 1) & 2) ? -cs : cs;
+  *s = sn;
+  *c = cs;
+}
+
 // e^x: n = rint(x log2 e), r = x - n ln2 (two-part ln2, exact first step),
 // Taylor on r, then 2^n applied as two normal factors so results down to the
 // subnormal range and up to overflow come out right without branches.
@@ -127,14 +162,14 @@ HK_HD double exp(double x) {
 
 // Kernel entry points; -DHK_MATH_LIBDEVICE selects CUDA's own sincospi/exp
 // (for A/B measurements).
-// sincospi for the generator: libdevice and hk::math::sincospi measured equal
-// on B200 (2.305 vs 2.315 ms per 1e8 events), so libdevice is the default;
-// -DHK_MATH_OWN_SINCOSPI selects ours.
+// sincospi for the generator: sincospi_gen (minimax, ~30 instructions) by
+// default; -DHK_MATH_LIBDEVICE_SINCOSPI selects libdevice's for A/B.  (The
+// earlier Taylor-form sincospi measured equal to libdevice: 2.315 vs 2.305 ms.)
 HK_HD void k_sincospi(double t, double* s, double* c) {
-#if defined(__CUDA_ARCH__) && !defined(HK_MATH_OWN_SINCOSPI)
+#if defined(__CUDA_ARCH__) && defined(HK_MATH_LIBDEVICE_SINCOSPI)
   ::sincospi(t, s, c);
 #else
-  sincospi(t, s, c);
+  sincospi_gen(t, s, c);
 #endif
 }
 

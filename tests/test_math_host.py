@@ -19,4 +19,5 @@ def test_device_math_accuracy(tmp_path):
                                     check=True).stdout)
     assert out["special_ok"], out
     assert out["sincospi_max_abs_err_ulp1"] <= 2.0, out   # absolute, in ulp(1) = 2.2e-16
+    assert out["sincospi_gen_max_abs_err_ulp1"] <= 2.0, out
     assert out["exp_max_rel_err_ulp"] <= 2.0, out
