@@ -61,3 +61,24 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def fit_exp(nterms: int):
+    """exp(r) on |r| <= ln2/2 as sum c_k r^k (near-minimax), for the FCN's
+    factored density (hk_fcn.cu fcn_exp_neg)."""
+    half = mp.log(2) / 2
+    xs = [half * mp.cos(mp.pi * (2 * i + 1) / 800) for i in range(400)]
+    w = [mp.mpf(1)] * len(xs)
+    for _ in range(30):
+        A = mp.matrix(len(xs), nterms)
+        y = mp.matrix(len(xs), 1)
+        for i, x in enumerate(xs):
+            sw = mp.sqrt(w[i])
+            for k in range(nterms):
+                A[i, k] = sw * x ** k
+            y[i] = sw * mp.exp(x)
+        c = mp.lu_solve(A.T * A, A.T * y)
+        err = [abs(mp.exp(x) - sum(c[k] * x ** k for k in range(nterms))) / mp.exp(x) for x in xs]
+        tot = sum(wi * ei for wi, ei in zip(w, err))
+        w = [wi * ei / tot for wi, ei in zip(w, err)]
+    return [c[k] for k in range(nterms)], max(err)
