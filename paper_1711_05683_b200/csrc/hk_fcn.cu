@@ -44,35 +44,6 @@ constexpr int kFcnFactored = 2;  // Gaussian + exponential, one exp per event
 // per 1e7 events) -- LDS latency in the dependency chain -- and was dropped.
 __device__ __forceinline__ double fcn_exp(double v) { return ::exp(v); }
 
-// e^d for d <= 0, the factored density's t = e^(min - max).  Inputs below
-// -708 are clamped: the term t scales is then below 1e-300 of the other, which
-// cannot move s given the host's amp window (NaN d also lands here; the
-// caller's exponent window rejects that row anyway).  n = rint(d log2 e),
-// r = d - n ln2 with a two-part ln2, a degree-10 near-minimax polynomial on
-// |r| <= ln2/2 (2.1e-16 relative, tools/fit_sincospi.py fit_exp), and 2^n
-// through the exponent field (n >= -1021: normal).  No special-case
-// branches, yet measured SLOWER in k_nll_fused on B200 (33.9 vs 29.0 us per
-// 1e7 events): its constants push the 64-register kernel into 96 B of
-// spills.  Kept for the record; density_factored uses libdevice's exp.
-__device__ __forceinline__ double fcn_exp_neg(double d) {
-  d = fmax(d, -708.0);
-  const double n = rint(d * 1.4426950408889634);
-  double r = fma(-n, 6.93147180369123816490e-01, d);  // ln2_hi: n * ln2_hi exact
-  r = fma(-n, 1.90821492927058770002e-10, r);         // ln2_lo
-  double p = 0x1.27288108f377dp-22;
-  p = fma(p, r, 0x1.72f9879b1dd67p-19);
-  p = fma(p, r, 0x1.a01b6be27d908p-16);
-  p = fma(p, r, 0x1.a0197a4c16f4bp-13);
-  p = fma(p, r, 0x1.6c16c0c117337p-10);
-  p = fma(p, r, 0x1.1111112d4a5eep-7);
-  p = fma(p, r, 0x1.5555555593186p-5);
-  p = fma(p, r, 0x1.555555554bc01p-3);
-  p = fma(p, r, 0x1.ffffffffffe18p-2);
-  p = fma(p, r, 0x1.000000000001dp+0);
-  p = fma(p, r, 1.0);
-  return p * __longlong_as_double((long long)((int)n + 1023) << 52);
-}
-
 __device__ __forceinline__ double density(const Coeffs& c, double x) {
   double d = 0.0;
 #pragma unroll 1
@@ -193,19 +164,10 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
     for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
 #pragma unroll
     for (int i = 0; i < kFcnRows; ++i) fcn_row<V>(c, xv[i], r0 + i * kBlock, lp, msum, bad);
-  } else {  // short range: groups of 4 loads in flight, stop at the CTA's last row
-    for (int i0 = 0; i0 < kFcnRows && begin + i0 * kBlock < end; i0 += 4) {
-      double xv[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t r = r0 + (i0 + k) * kBlock;
-        xv[k] = r < end ? __ldg(x + r) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t r = r0 + (i0 + k) * kBlock;
-        if (r < end) fcn_row<V>(c, xv[k], r, lp, msum, bad);
-      }
+  } else {  // the ragged last tile
+    for (int i = 0; i < kFcnRows; ++i) {
+      const int64_t r = r0 + i * kBlock;
+      if (r < end) fcn_row<V>(c, __ldg(x + r), r, lp, msum, bad);
     }
   }
   return V == kFcnFactored ? lp.value() + msum : lp.value();
