@@ -32,10 +32,15 @@ struct GenArgs {
   double* cols[kMaxCols];  // all NULL = no store
   double* wpart;           // 2 doubles per warp-slice (HK_WARP_SLICES per chunk) or NULL
   int store;
+  int vec2;                // all columns 16-byte aligned: double2 stores (k_generate VEC2)
 };
 
 // ------------------------------------------------------------ generation ---
-template <int N, int MODE>
+// VEC2: every column pointer is 16-byte aligned, so the two adjacent rows a
+// thread owns in the ILP-2 path go out as one 16-byte streaming store per
+// column (st.global.cs.v2.f64; a warp writes 512 contiguous bytes).  The row
+// mapping -- and so the weight partials -- is the same either way.
+template <int N, int MODE, bool VEC2>
 __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
     k_generate(const __grid_constant__ GenArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
@@ -44,22 +49,30 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
                                   a.d.m_mother);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
-    // full chunks, mother at rest: rows r and r + 2048 together (ILP 2)
+    // full chunks, mother at rest: rows 2t and 2t + 1 of each 512-row block
+    // together (ILP 2)
     if (GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {
-        const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
-        const int64_t r1 = r0 + HK_CHUNK / 2;
+        const int64_t r0 = c * HK_CHUNK + i * (2 * kBlock) + 2 * threadIdx.x;
+        const int64_t r1 = r0 + 1;
         double p0[4 * N], p1[4 * N];
         const double w0 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r0, p0);
         const double w1 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r1, p1);
         if (a.store) {
-          __stcs(a.cols[0] + r0, w0);
-          __stcs(a.cols[0] + r1, w1);
+          if constexpr (VEC2) {
+            __stcs(reinterpret_cast<double2*>(a.cols[0] + r0), make_double2(w0, w1));
 #pragma unroll
-          for (int j = 0; j < 4 * N; ++j) {
-            __stcs(a.cols[1 + j] + r0, p0[j]);
-            __stcs(a.cols[1 + j] + r1, p1[j]);
+            for (int j = 0; j < 4 * N; ++j)
+              __stcs(reinterpret_cast<double2*>(a.cols[1 + j] + r0), make_double2(p0[j], p1[j]));
+          } else {
+            __stcs(a.cols[0] + r0, w0);
+            __stcs(a.cols[0] + r1, w1);
+#pragma unroll
+            for (int j = 0; j < 4 * N; ++j) {
+              __stcs(a.cols[1 + j] + r0, p0[j]);
+              __stcs(a.cols[1 + j] + r1, p1[j]);
+            }
           }
         }
         acc[0] += w0;
@@ -549,8 +562,13 @@ int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStre
 template <int MODE>
 int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
   switch (a.d.n) {
-#define HK_GEN_CASE(NN) \
-  case NN: k_generate<NN, MODE><<<grid, kBlock, 0, st>>>(a); break;
+#define HK_GEN_CASE(NN)                                              \
+  case NN:                                                           \
+    if (NN <= 4 && a.vec2)                                           \
+      k_generate<NN, MODE, (NN <= 4)><<<grid, kBlock, 0, st>>>(a);   \
+    else                                                             \
+      k_generate<NN, MODE, false><<<grid, kBlock, 0, st>>>(a);       \
+    break;
     HK_GEN_CASE(2)
     HK_GEN_CASE(3)
     HK_GEN_CASE(4)
@@ -721,9 +739,11 @@ int hk_phsp_generate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_be
   a.wpart = d_wpartials;
   a.store = d_cols != nullptr;
   if (d_cols) {
+    a.vec2 = 1;
     for (int j = 0; j < 4 * spec->n + 1; ++j) {
       HK_REQUIRE(d_cols[j] != nullptr, "column %d is NULL", j);
       a.cols[j] = d_cols[j];
+      if (reinterpret_cast<uintptr_t>(d_cols[j]) % 16) a.vec2 = 0;
     }
   }
   HK_REQUIRE(a.store || a.wpart, "nothing to write (no columns, no partials)");
