@@ -524,6 +524,20 @@ def run_ours(args) -> None:
                "steps": e_steps}
         if dist:
             e2e["value"] = n_total / _max_over_ranks(torch, dist, e_dt)
+        # the ceiling this leg runs into: raw device->host copy into pinned memory
+        raw = host[0].view(torch.uint8)
+        dev_src = torch.empty(raw.numel(), dtype=torch.uint8, device="cuda")
+        raw.copy_(dev_src)
+        torch.cuda.synchronize()
+        c0 = time.perf_counter()
+        for _ in range(3):
+            raw.copy_(dev_src, non_blocking=True)
+        torch.cuda.synchronize()
+        ceiling = 3 * raw.numel() / (time.perf_counter() - c0) / 1e9
+        e2e["d2h_ceiling_GBps"] = ceiling
+        e2e["d2h_GBps"] = (BYTES_PER_EVENT * n + 16) / e_dt / 1e9
+        e2e["frac_of_d2h_ceiling"] = e2e["d2h_GBps"] / ceiling
+        del dev_src, raw
         del host
 
     others = None if args.no_configs else other_configs(hk, torch, _lib, rank, world, dist)
