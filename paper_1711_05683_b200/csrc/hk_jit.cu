@@ -162,26 +162,36 @@ struct JitArgs {
 // Chunk moments: the per-thread order and block tree of k_moments /
 // block_sum_store<5> (hk_phsp.cu, hk_device.cuh).
 const char* kStoredKernels = R"(
+__device__ __forceinline__ void hk_row_moments(const JitArgs& a, long long r, double (&acc)[5]) {
+  bool d0 = false;
+  const double f = hk_f(a, r, d0);
+  if (d0 && a.div0) atomicMin(a.div0, (u64)r);
+  if (!isfinite(f) && a.nonfin) atomicMin(a.nonfin, (u64)r);
+  const double w = __ldg(a.cols[0] + r);
+  const double ww = __dmul_rn(w, w);
+  acc[0] = __dadd_rn(acc[0], w);
+  acc[1] = __dadd_rn(acc[1], __dmul_rn(w, f));
+  acc[2] = __dadd_rn(acc[2], ww);
+  acc[3] = __dadd_rn(acc[3], __dmul_rn(ww, f));
+  acc[4] = __dadd_rn(acc[4], __dmul_rn(__dmul_rn(ww, f), f));
+}
+
 extern "C" __global__ void __launch_bounds__(256) hk_jit_moments(const __grid_constant__ JitArgs a) {
   __shared__ double sm[8][5];
   const long long chunks = (a.count + 4095) / 4096;
   for (long long c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-      const long long r = c * 4096 + i * 256 + threadIdx.x;
-      if (r < a.count) {
-        bool d0 = false;
-        const double f = hk_f(a, r, d0);
-        if (d0 && a.div0) atomicMin(a.div0, (u64)r);
-        if (!isfinite(f) && a.nonfin) atomicMin(a.nonfin, (u64)r);
-        const double w = __ldg(a.cols[0] + r);
-        const double ww = __dmul_rn(w, w);
-        acc[0] = __dadd_rn(acc[0], w);
-        acc[1] = __dadd_rn(acc[1], __dmul_rn(w, f));
-        acc[2] = __dadd_rn(acc[2], ww);
-        acc[3] = __dadd_rn(acc[3], __dmul_rn(ww, f));
-        acc[4] = __dadd_rn(acc[4], __dmul_rn(__dmul_rn(ww, f), f));
+    // full chunk: no guards, two rows' loads in flight.  Measured on B200 for
+    // <m12^2> over 1e8 stored rows: unroll 1 / 2 / 4 / 8 = 1.31 / 1.16 /
+    // 1.27 / 1.37 ms (more unrolling costs resident warps)
+    if (c * 4096 + 4096 <= a.count) {
+#pragma unroll 2
+      for (int i = 0; i < 16; ++i) hk_row_moments(a, c * 4096 + i * 256 + threadIdx.x, acc);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < 16; ++i) {
+        const long long r = c * 4096 + i * 256 + threadIdx.x;
+        if (r < a.count) hk_row_moments(a, r, acc);
       }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
