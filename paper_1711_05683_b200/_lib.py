@@ -243,8 +243,9 @@ def ptr_rows(block) -> ctypes.Array:
 
 
 def empty(n: int, dtype=None):
+    _require_device()
     t = torch()
-    return t.empty(int(n), dtype=dtype or t.float64, device=device())
+    return t.empty(int(n), dtype=dtype or t.float64, device="cuda")   # the current device
 
 
 def bad_cells(k: int = 1):
