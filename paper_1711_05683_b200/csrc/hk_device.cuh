@@ -374,6 +374,59 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
   return w;
 }
 
+// A 2-body decay at rest has every per-event quantity but the direction
+// fixed by the decay: breakup momentum (= the weight), cluster energy, the
+// frame's gamma, 1/E and gamma^2/(gamma+1), and daughter 2's energy.
+// two_body_consts computes them ONCE per thread with exactly the operations
+// of rest_event<2>; rest_event2 then spends per event only the RNG, the
+// direction and the boost -- the outputs are bit-identical to rest_event<2>.
+// (Used for chain sub-decays such as J/psi -> mu mu.)
+struct TwoBody {
+  double w, q, r, gamma, g2, e2, m0;
+};
+
+__device__ __forceinline__ TwoBody two_body_consts(const hk_decay_t& d) {
+  TwoBody t;
+  const double inv0 = d.csum[0];        // 0 * T + csum[0] is exact
+  const double inv1 = d.T + d.csum[1];  // phasespace.py:118
+  t.q = pstar(inv1, inv0, d.masses[1] * d.masses[1]);
+  t.w = 1.0 * t.q;
+  const double cle = fast_sqrt(t.q * t.q + inv0 * inv0);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  t.gamma = inv0 == 0.0 ? cle * inf : cle * fast_rcp(inv0);
+  t.r = fast_rcp(cle);
+  t.g2 = t.gamma * t.gamma * fast_rcp(t.gamma + 1.0);
+  t.e2 = fast_sqrt(t.q * t.q + d.masses[1] * d.masses[1]);
+  t.m0 = d.masses[0];
+  return t;
+}
+
+template <int MODE>
+__device__ __forceinline__ double rest_event2(const TwoBody& t, const RngParams& rp, uint64_t row,
+                                              double (&p)[8]) {
+  uint64_t bits[2];
+  draw_bits<2, MODE>(rp, row, bits);
+  const double cz = two_unit_minus_one(bits[0]);
+  const double two_u = two_unit(bits[1]);
+  const double sz = fast_sqrt(1.0 - cz * cz);
+  double sn, cs;
+  math::k_sincospi(two_u, &sn, &cs);
+  const double nx = sz * cs, ny = sz * sn, nz = cz;
+  const double clx = t.q * nx, cly = t.q * ny, clz = t.q * nz;
+  Frame f;
+  f.gamma = t.gamma;
+  f.bx = clx * t.r;
+  f.by = cly * t.r;
+  f.bz = clz * t.r;
+  f.g2 = t.g2;
+  boost_rest(f, t.m0, p[0], p[1], p[2], p[3]);
+  p[4] = t.e2;
+  p[5] = -clx;
+  p[6] = -cly;
+  p[7] = -clz;
+  return t.w;
+}
+
 // Runtime-n variant (n <= HK_MAX_DAUGHTERS); arrays live in local memory.
 template <int MODE>
 __device__ double rest_event_rt(const hk_decay_t& d, const RngParams& rp, uint64_t row,

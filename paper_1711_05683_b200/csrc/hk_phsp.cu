@@ -36,6 +36,16 @@ struct GenArgs {
 };
 
 // ------------------------------------------------------------ generation ---
+// one event at rest; 2-body decays take the hoisted-constant form (same bits)
+template <int N, int MODE>
+__device__ __forceinline__ double gen_event(const hk_decay_t& d, const TwoBody& tb, const RngParams& rp,
+                                           uint64_t row, double (&p)[4 * N]) {
+  if constexpr (N == 2)
+    return rest_event2<MODE>(tb, rp, row, p);
+  else
+    return rest_event<N, MODE>(d, rp, row, p);
+}
+
 // VEC2: every column pointer is 16-byte aligned, so the two adjacent rows a
 // thread owns in the ILP-2 path go out as one 16-byte streaming store per
 // column (st.global.cs.v2.f64; a warp writes 512 contiguous bytes).  The row
@@ -47,6 +57,8 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
                                   a.d.m_mother);
+  TwoBody tb{};
+  if constexpr (N == 2) tb = two_body_consts(a.d);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
     // full chunks, mother at rest: rows 2t and 2t + 1 of each 512-row block
@@ -57,8 +69,8 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         const int64_t r0 = c * HK_CHUNK + i * (2 * kBlock) + 2 * threadIdx.x;
         const int64_t r1 = r0 + 1;
         double p0[4 * N], p1[4 * N];
-        const double w0 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r0, p0);
-        const double w1 = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r1, p1);
+        const double w0 = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r0, p0);
+        const double w1 = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r1, p1);
         if (a.store) {
           if constexpr (VEC2) {
             __stcs(reinterpret_cast<double2*>(a.cols[0] + r0), make_double2(w0, w1));
@@ -88,7 +100,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
       const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
       if (r < a.count) {
         double p[4 * N];
-        const double w = rest_event<N, MODE>(a.d, a.rp, a.ev_begin + (uint64_t)r, p);
+        const double w = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r, p);
         if (a.d.moving) {
 #pragma unroll
           for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
@@ -233,6 +245,8 @@ __device__ __forceinline__ bool mass_mismatch(double fm, double M) {
 template <int NS, int MODE>
 __global__ void __launch_bounds__(kBlock) k_chain(const __grid_constant__ ChainArgs a) {
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
+  TwoBody tb{};
+  if constexpr (NS == 2) tb = two_body_consts(a.sub);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
 #pragma unroll 1
     for (int i = 0; i < kRowsPerThread; ++i) {
@@ -244,7 +258,11 @@ __global__ void __launch_bounds__(kBlock) k_chain(const __grid_constant__ ChainA
       const double fm = frame_mass(fe, fx, fy, fz);
       if (mass_mismatch(fm, a.sub.mother_mass)) record_bad(a.first_bad, row);
       double q[4 * NS];
-      const double ws = rest_event<NS, MODE>(a.sub, a.rp, row, q);
+      double ws;
+      if constexpr (NS == 2)
+        ws = rest_event2<MODE>(tb, a.rp, row, q);
+      else
+        ws = rest_event<NS, MODE>(a.sub, a.rp, row, q);
       const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
 #pragma unroll
       for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
@@ -295,8 +313,8 @@ __device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a, in
 // K >= 0: the decaying daughter as a compile-time index (the hot 3-body
 // parent), so its four-vector is a register reference instead of a select chain.
 template <int N, int NS, int MODE, int K>
-__device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, int64_t r,
-                                            unsigned long long* bad) {
+__device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, const TwoBody& tb,
+                                            int64_t r, unsigned long long* bad) {
   const int k = K >= 0 ? K : a.k;
   const uint64_t row = a.ev_begin + (uint64_t)r;
   double p[4 * N];
@@ -326,7 +344,11 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
   const double fm = frame_mass(fe, fx, fy, fz);
   *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
   double q[4 * NS];
-  const double ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
+  double ws;
+  if constexpr (NS == 2)
+    ws = rest_event2<MODE>(tb, a.rp_sub, row, q);  // per-launch constants hoisted, same bits
+  else
+    ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
   const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
 #pragma unroll
   for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
@@ -357,14 +379,16 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
                                   a.d.m_mother);
   unsigned long long bad = ~0ull;
+  TwoBody tb{};
+  if constexpr (NS == 2) tb = two_body_consts(a.sub);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
     if (HK_CHAIN_ILP == 2 && N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
         const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
-        const double w0 = chain_row<N, NS, MODE, K>(a, mf, r0, &bad);
-        const double w1 = chain_row<N, NS, MODE, K>(a, mf, r0 + HK_CHUNK / 2, &bad);
+        const double w0 = chain_row<N, NS, MODE, K>(a, mf, tb, r0, &bad);
+        const double w1 = chain_row<N, NS, MODE, K>(a, mf, tb, r0 + HK_CHUNK / 2, &bad);
         acc[0] += w0;
         acc[1] += w0 * w0;
         acc[0] += w1;
@@ -375,7 +399,7 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
       for (int i = 0; i < kRowsPerThread; ++i) {
         const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
         if (r < a.count) {
-          const double w = chain_row<N, NS, MODE, K>(a, mf, r, &bad);
+          const double w = chain_row<N, NS, MODE, K>(a, mf, tb, r, &bad);
           acc[0] += w;
           acc[1] += w * w;
         }
