@@ -474,8 +474,9 @@ def run_ours(args) -> None:
         _lib.check(L.hk_phsp_generate(d, k, rank * n, n, colp, _lib.ptr(wpart), st.cuda_stream), "generate")
         if gen_events:
             gen_events[1].record(st)
-        full = gather_partials(wpart, n_total, 2 * _lib.HK_WARP_SLICES)   # per chunk: 8 slices x 2
-        return _lib.fold(full, _lib.num_weight_slices(n_total), 2)
+        local = _lib.weight_chunk_partials(wpart, n)     # per chunk: 8 warp slices -> 1 pair
+        full = gather_partials(local, n_total, 2)          # 16 B per chunk cross GPUs
+        return _lib.fold(full, _lib.num_chunks(n_total), 2)
 
     for _ in range(args.warmup):
         tot = step()
@@ -581,7 +582,7 @@ def run_ours(args) -> None:
                          "kernel_ms": gen_avg * 1e3, "kernel_share_of_step": gen_avg / per_step},
             "clocks": clocks.summary(),
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 3 * args.steps,   # k_generate + k_fold_segments + k_fold per step
             "cpu_baseline": cpu,
             "fcn": fcn,
             "other_configs": others,

@@ -243,6 +243,14 @@ int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_b
                       int64_t ev_count, const hk_program_t* f, const hk_pair_integrand_t* pair,
                       double* d_partials, uint64_t* d_first_bad, void* stream);
 
+/* Fixed-order fold of each segment of seg_len consecutive partials (width
+ * doubles each) into one: d_out[s * width + w] = sum over j ascending of
+ * d_partials[(s * seg_len + j) * width + w].  Used to turn a chunk's
+ * HK_WARP_SLICES weight partials into one chunk partial before partials cross
+ * GPUs, so the global fold sees the same chunk sequence at any GPU count. */
+int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_len, int32_t width,
+                     double* d_out, void* stream);
+
 /* Deterministic fold of n_parts partials of `width` (<= 32) doubles each
  * (parallel.py:86-92 semantics, fixed tree order) into d_out[width]. */
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,

@@ -41,7 +41,7 @@ EXPORTS = (
     "hk_yield_partials", "hk_splot_weights",
     "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
     "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
-    "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles",
+    "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles", "hk_fold_segments",
 )
 
 
@@ -132,6 +132,7 @@ _SIGS = {
     "hk_jit_compile": (_INT, [_F, _I32, _I32, ctypes.POINTER(_I64)]),
     "hk_csv_scratch_bytes": (_I64, [_I64, _I32]),
     "hk_nll_work_doubles": (_I64, [_I64]),
+    "hk_fold_segments": (_INT, [_P, _I64, _I32, _I32, _P, _P]),
     "hk_format_csv": (_INT, [_PP, _I32, _I64, _P, _P, _I64, ctypes.POINTER(_I64), _P]),
 }
 
@@ -314,6 +315,26 @@ def fold(partials, n_parts: int, width: int):
     check(lib().hk_fold_partials(ptr(partials) if n_parts else None, int(n_parts), int(width),
                                  ptr(out), stream_ptr()), "hk_fold_partials")
     return out
+
+
+def fold_segments(partials, n_segments: int, seg_len: int, width: int):
+    """Fixed-order fold of each run of seg_len partials -> (n_segments, width)."""
+    out = empty(max(int(n_segments), 0) * width)
+    if n_segments:
+        check(lib().hk_fold_segments(ptr(partials), int(n_segments), int(seg_len), int(width), ptr(out),
+                                     stream_ptr()), "hk_fold_segments")
+    return out
+
+
+def weight_chunk_partials(wpart, n: int):
+    """A generation's per-warp-slice (sum w, sum w^2) -> one pair per 4096-row
+    chunk (the records that cross GPUs); fold them with fold(., num_chunks(n), 2)."""
+    return fold_segments(wpart, num_chunks(n), HK_WARP_SLICES, 2)
+
+
+def weight_totals(wpart, n: int):
+    """(sum w, sum w^2) of a generation: slices -> chunks -> total, fixed order."""
+    return fold(weight_chunk_partials(wpart, n), num_chunks(n), 2)
 
 
 JIT_OFF, JIT_ALWAYS, JIT_AUTO = 0, 1, 2

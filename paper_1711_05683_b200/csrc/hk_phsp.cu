@@ -585,6 +585,30 @@ int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStre
   return check_launch("k_fold");
 }
 
+// Per-segment fold in fixed order: out[s][w] = sum_j parts[s * seg_len + j][w],
+// j ascending -- e.g. a chunk's 8 warp-slice weight partials into one chunk
+// partial, so that only per-chunk records cross GPUs (8x fewer bytes) and the
+// global fold sees the same chunk sequence at any GPU count.
+__global__ void __launch_bounds__(256) k_fold_segments(const double* __restrict__ parts, int64_t n_seg,
+                                                       int seg_len, int width, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * 256ll + threadIdx.x;
+  if (i >= n_seg * width) return;
+  const int64_t s = i / width;
+  const int w = (int)(i - s * width);
+  const double* p = parts + s * seg_len * width + w;
+  double acc = __ldg(p);
+  for (int j = 1; j < seg_len; ++j) acc += __ldg(p + (int64_t)j * width);
+  out[i] = acc;
+}
+
+int launch_fold_segments(const double* parts, int64_t n_seg, int seg_len, int width, double* out,
+                         cudaStream_t st) {
+  if (n_seg <= 0) return HK_OK;
+  const int64_t threads = n_seg * width;
+  k_fold_segments<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(parts, n_seg, seg_len, width, out);
+  return check_launch("k_fold_segments");
+}
+
 // ------------------------------------------------------ launch dispatch ----
 template <int MODE>
 int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
@@ -958,6 +982,15 @@ int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_b
   }
   return key->mode == HK_RNG_REFERENCE ? dispatch_integrate<HK_RNG_REFERENCE>(a, grid, st)
                                        : dispatch_integrate<HK_RNG_PHILOX>(a, grid, st);
+}
+
+int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_len, int32_t width,
+                     double* d_out, void* stream) {
+  HK_REQUIRE(width >= 1 && width <= 32 && seg_len >= 1 && seg_len <= 1024, "bad segment shape %d x %d",
+             seg_len, width);
+  HK_REQUIRE(n_segments >= 0, "negative segment count");
+  HK_REQUIRE(n_segments == 0 || (d_partials && d_out), "NULL pointer");
+  return launch_fold_segments(d_partials, n_segments, seg_len, width, d_out, as_stream(stream));
 }
 
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,

@@ -29,6 +29,8 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 int launch_fold(const double* parts, int64_t n, int width, double* out, cudaStream_t st);
+int launch_fold_segments(const double* parts, int64_t n_seg, int seg_len, int width, double* out,
+                         cudaStream_t st);
 
 // One copy stream + two events per device, created on first use.
 struct CopyLane {
@@ -92,8 +94,9 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
   const int ncols = 4 * spec->n + 1;
   const int64_t chunks = num_chunks(ev_count);
-  // stage layout: [partials: 2 doubles per warp-slice][sum cell: 2 doubles][2 x piece buffers]
-  const size_t head = (size_t)(chunks * 2 * HK_WARP_SLICES + 2) * sizeof(double);
+  // stage layout: [partials: 2 doubles per warp-slice][chunk partials: 2 per chunk]
+  //               [sum cell: 2 doubles][2 x piece buffers]
+  const size_t head = (size_t)(chunks * 2 * HK_WARP_SLICES + chunks * 2 + 2) * sizeof(double);
   HK_REQUIRE(stage_bytes > head, "staging area too small");
   const size_t per_row = (size_t)ncols * sizeof(double);
   int64_t piece = (int64_t)((stage_bytes - head) / (2 * per_row));
@@ -107,7 +110,8 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
   if (int rc = copy_lane(&L)) return rc;
   cudaStream_t st = as_stream(stream);
   double* part = static_cast<double*>(d_stage);
-  double* sums = part + chunks * 2 * HK_WARP_SLICES;
+  double* cpart = part + chunks * 2 * HK_WARP_SLICES;
+  double* sums = cpart + chunks * 2;
   double* buf[2] = {sums + 2, sums + 2 + piece * ncols};
   for (int64_t off = 0, i = 0; off < ev_count; off += piece, ++i) {
     const int b = (int)(i & 1);
@@ -125,7 +129,9 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
                               cudaMemcpyDeviceToHost, L->copy));
     HK_CUDA(cudaEventRecord(L->freed[b], L->copy));
   }
-  if (int rc = launch_fold(part, chunks * HK_WARP_SLICES, 2, sums, st)) return rc;
+  // the same two-level fold as phsp_weight_moments: slices -> chunks -> total
+  if (int rc = launch_fold_segments(part, chunks, HK_WARP_SLICES, 2, cpart, st)) return rc;
+  if (int rc = launch_fold(cpart, chunks, 2, sums, st)) return rc;
   HK_CUDA(cudaStreamSynchronize(L->copy));
   if (h_wsums) {
     HK_CUDA(cudaMemcpyAsync(h_wsums, sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));

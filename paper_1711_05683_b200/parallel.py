@@ -92,8 +92,11 @@ def gather_partials(local, n_total: int, width: int, group=None):
 def sharded_weight_moments(block_shard, n_total: int, group=None):
     """Global (sum w, sum w^2) of a sharded generation: gather + same fold."""
     parts = block_shard.meta["weight_partials"]   # 2 doubles per warp-slice, 8 slices per chunk
-    full = gather_partials(parts, n_total, 2 * _lib.HK_WARP_SLICES, group)
-    return _lib.fold(full, _lib.num_weight_slices(n_total), 2)
+    # fold each chunk's 8 slices locally (fixed order), so only one record per
+    # chunk crosses GPUs; every rank then folds the same global chunk sequence
+    local = _lib.weight_chunk_partials(parts, len(block_shard))
+    full = gather_partials(local, n_total, 2, group)
+    return _lib.fold(full, _lib.num_chunks(n_total), 2)
 
 
 def sharded_integrate(expr, spec, mother, n_total: int, key, arg_builder, group=None,

@@ -141,7 +141,7 @@ def phsp_generate_to_host(spec: DecaySpec, mother: FourVector, n_events: int, ke
     ncols = 4 * spec.n + 1
     if out is None:
         out = [torch.empty(n_events, dtype=torch.float64, pin_memory=True) for _ in range(ncols)]
-    head = (2 * _lib.num_weight_slices(n_events) + 2) * 8
+    head = (2 * _lib.num_weight_slices(n_events) + 2 * _lib.num_chunks(n_events) + 2) * 8
     stage_bytes = max(int(stage_bytes), head + 2 * ncols * 8 * _lib.HK_CHUNK)
     stage = _stage_buffer(stage_bytes)
     sums = (ctypes.c_double * 2)()
@@ -209,7 +209,7 @@ def phsp_weight_moments(block: ColumnStore) -> WeightMoments:
         parts5 = _moment_partials(block, prog)
         tot = _lib.fold(parts5, _lib.num_chunks(n), 5).cpu().numpy()
         return WeightMoments(n, float(tot[0]), float(tot[2]))
-    tot = _lib.fold(parts, _lib.num_weight_slices(n), 2).cpu().numpy()
+    tot = _lib.weight_totals(parts, n).cpu().numpy()
     return WeightMoments(n, float(tot[0]), float(tot[1]))
 
 

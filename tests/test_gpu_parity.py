@@ -493,14 +493,14 @@ def test_sharded_runs_bitwise_invariant(cuda, hk):
     spec, mother = _b0(hk)
     n = 2_000_003
     one = hk.phsp_generate(spec, mother, n, hk.RngKey(1, 1))
-    ref_tot = _lib.fold(one.meta["weight_partials"], _lib.num_weight_slices(n), 2).cpu().numpy()
+    ref_tot = _lib.weight_totals(one.meta["weight_partials"], n).cpu().numpy()
     for world in (2, 4, 8):
         parts, cols = [], []
         for r in range(world):
             a, b = shard_range(n, r, world)
             s = hk.phsp_generate(spec, mother, b - a, hk.RngKey(1, 1), row_offset=a)
-            parts.append(s.meta["weight_partials"])
+            parts.append(_lib.weight_chunk_partials(s.meta["weight_partials"], b - a))
             cols.append(s.device_column("p2_px"))
         assert torch.equal(torch.cat(cols), one.device_column("p2_px"))
-        tot = _lib.fold(torch.cat(parts), _lib.num_weight_slices(n), 2).cpu().numpy()
+        tot = _lib.fold(torch.cat(parts), _lib.num_chunks(n), 2).cpu().numpy()
         assert np.array_equal(tot, ref_tot), world
