@@ -72,6 +72,8 @@ def test_every_entry_point_marshals_and_validates(hk):
     assert L.hk_compact(cols, 13, 0, dp, dp, cols, 0, None) == OK
     lo = (ctypes.c_double * 1)(0.0)
     assert L.hk_sample_pdf(prog, 1, lo, lo, 1.0, k, 0, 0, 10, cols, dp, None) == OK
+    assert L.hk_fold_segments(None, 0, 8, 2, None, None) == OK
+    assert L.hk_fold_segments(dp, 4, 0, 2, dp, None) == _lib.HK_EINVAL
     assert L.hk_csv_scratch_bytes(0, 13) == 0
     assert L.hk_csv_scratch_bytes(1000, 13) > 1000 * 13 * 24
     text_len = ctypes.c_int64(-1)
