@@ -231,6 +231,20 @@ __device__ __forceinline__ Frame make_frame_fast(double fe, double fx, double fy
   return f;
 }
 
+// make_frame_fast with fast_rcp(fm) supplied (a frame whose mass is fixed)
+__device__ __forceinline__ Frame make_frame_fast_r(double fe, double fx, double fy, double fz,
+                                                   double fm, double rcp_fm) {
+  Frame f;
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  f.gamma = fm == 0.0 ? fe * inf : fe * rcp_fm;
+  const double r = fast_rcp(fe);
+  f.bx = fx * r;
+  f.by = fy * r;
+  f.bz = fz * r;
+  f.g2 = f.gamma * f.gamma * fast_rcp(f.gamma + 1.0);
+  return f;
+}
+
 // _boost with the multiply-adds fused (the translation unit has -fmad=false,
 // so contraction is opt-in here and nowhere else).
 __device__ __forceinline__ void boost_fma(const Frame& f, double& e, double& px, double& py,
@@ -298,6 +312,21 @@ __device__ __forceinline__ double pstar(double M, double a, double b2) {
   return cr_div(sqrt_lambda(lam), 2.0 * M);
 }
 
+// cr_div with the divisor's reciprocal supplied (r = fast_rcp(b), hoisted)
+__device__ __forceinline__ double cr_div_r(double a, double b, double r) {
+  const double q = a * r;
+  const double rem = fma(-b, q, a);
+  return fma(rem, r, q);
+}
+
+// pstar with 1/(2M) supplied (the last breakup of a decay, M fixed)
+__device__ __forceinline__ double pstar_r(double M, double a, double b2, double rcp_2m) {
+  const double M2 = M * M, a2 = a * a;
+  const double t = (M2 - a2) - b2;
+  const double lam = t * t - (4.0 * a2) * b2;
+  return cr_div_r(sqrt_lambda(lam), 2.0 * M, rcp_2m);
+}
+
 // c ? a : b through PTX selp, opaque to the front end's array-index recovery
 __device__ __forceinline__ double select_f64(bool c, double a, double b) {
   double r;
@@ -317,9 +346,26 @@ __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
 // One event of the rest-frame generator (phasespace.py:103-149) for a
 // compile-time daughter count N.  p[4j..4j+3] = (e, px, py, pz) of daughter
 // j+1; returns the weight (product of breakup momenta, phasespace.py:120-125).
+// Per-decay reciprocals of rest_event<N>, hoistable out of the event loop
+// (computed with the very operations rest_event would use, so events are
+// bit-identical): 1/(2M) of the last breakup (M = inv[N-1] is fixed by the
+// decay) and 1/inv[0] of the first cluster frame.
+struct RestHoist {
+  double rcp_2m_last;
+  double rcp_inv0;
+};
+
+template <int N>
+__device__ __forceinline__ RestHoist rest_hoist(const hk_decay_t& d) {
+  RestHoist h;
+  h.rcp_2m_last = fast_rcp(2.0 * (d.T + d.csum[N - 1]));
+  h.rcp_inv0 = fast_rcp(d.csum[0]);
+  return h;
+}
+
 template <int N, int MODE>
 __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParams& rp,
-                                             uint64_t row, double (&p)[4 * N]) {
+                                             uint64_t row, double (&p)[4 * N], const RestHoist& h) {
   constexpr int D = 3 * N - 4;  // phasespace.py:84-86
   uint64_t bits[D];
   draw_bits<D, MODE>(rp, row, bits);
@@ -339,7 +385,8 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
   double w = 1.0;
 #pragma unroll
   for (int k = 1; k < N; ++k) {
-    ps[k] = pstar(inv[k], inv[k - 1], d.masses[k] * d.masses[k]);
+    ps[k] = k == N - 1 ? pstar_r(inv[k], inv[k - 1], d.masses[k] * d.masses[k], h.rcp_2m_last)
+                       : pstar(inv[k], inv[k - 1], d.masses[k] * d.masses[k]);
     w = w * ps[k];
   }
 
@@ -359,7 +406,8 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
     const double clm = inv[k - 1];
     const double cle = fast_sqrt(q * q + clm * clm);
     const double clx = q * nx, cly = q * ny, clz = q * nz;
-    const Frame f = make_frame_fast(cle, clx, cly, clz, clm);
+    const Frame f = k == 1 ? make_frame_fast_r(cle, clx, cly, clz, clm, h.rcp_inv0)
+                           : make_frame_fast(cle, clx, cly, clz, clm);
     if (k == 1) {
       boost_rest(f, d.masses[0], p[0], p[1], p[2], p[3]);  // daughter 1 starts at rest
     } else {
@@ -372,6 +420,12 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
     p[4 * k + 3] = -clz;
   }
   return w;
+}
+
+template <int N, int MODE>
+__device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParams& rp,
+                                             uint64_t row, double (&p)[4 * N]) {
+  return rest_event<N, MODE>(d, rp, row, p, rest_hoist<N>(d));
 }
 
 // A 2-body decay at rest has every per-event quantity but the direction

@@ -107,6 +107,7 @@ __device__ __forceinline__ void integrate_chunks(const IntArgs& a) {
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
                                   a.d.m_mother);
+  const RestHoist h = rest_hoist<N>(a.d);  // per-decay reciprocals, out of the event loop
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (I::kIlp2 && GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
@@ -115,8 +116,8 @@ __device__ __forceinline__ void integrate_chunks(const IntArgs& a) {
         const uint64_t row0 = a.ev_begin + (uint64_t)(c * HK_CHUNK + i * kBlock + threadIdx.x);
         const uint64_t row1 = row0 + HK_CHUNK / 2;
         double p0[4 * N], p1[4 * N];
-        const double w0 = rest_event<N, MODE>(a.d, a.rp, row0, p0);
-        const double w1 = rest_event<N, MODE>(a.d, a.rp, row1, p1);
+        const double w0 = rest_event<N, MODE>(a.d, a.rp, row0, p0, h);
+        const double w1 = rest_event<N, MODE>(a.d, a.rp, row1, p1, h);
         const double f0 = I::template eval<N>(a, w0, p0, row0);
         const double f1 = I::template eval<N>(a, w1, p1, row1);
         if (!isfinite(f0)) record_bad(a.nonfinite_bad, row0);
@@ -133,7 +134,7 @@ __device__ __forceinline__ void integrate_chunks(const IntArgs& a) {
       if (r < a.count) {
         const uint64_t row = a.ev_begin + (uint64_t)r;
         double p[4 * N];
-        const double w = rest_event<N, MODE>(a.d, a.rp, row, p);
+        const double w = rest_event<N, MODE>(a.d, a.rp, row, p, h);
         if (a.d.moving) {
 #pragma unroll
           for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);

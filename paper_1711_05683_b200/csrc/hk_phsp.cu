@@ -38,12 +38,12 @@ struct GenArgs {
 // ------------------------------------------------------------ generation ---
 // one event at rest; 2-body decays take the hoisted-constant form (same bits)
 template <int N, int MODE>
-__device__ __forceinline__ double gen_event(const hk_decay_t& d, const TwoBody& tb, const RngParams& rp,
-                                           uint64_t row, double (&p)[4 * N]) {
+__device__ __forceinline__ double gen_event(const hk_decay_t& d, const TwoBody& tb, const RestHoist& h,
+                                           const RngParams& rp, uint64_t row, double (&p)[4 * N]) {
   if constexpr (N == 2)
     return rest_event2<MODE>(tb, rp, row, p);
   else
-    return rest_event<N, MODE>(d, rp, row, p);
+    return rest_event<N, MODE>(d, rp, row, p, h);
 }
 
 // VEC2: every column pointer is 16-byte aligned, so the two adjacent rows a
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
                                   a.d.m_mother);
   TwoBody tb{};
   if constexpr (N == 2) tb = two_body_consts(a.d);
+  const RestHoist h = rest_hoist<N>(a.d);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
     // full chunks, mother at rest: rows 2t and 2t + 1 of each 512-row block
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         const int64_t r0 = c * HK_CHUNK + i * (2 * kBlock) + 2 * threadIdx.x;
         const int64_t r1 = r0 + 1;
         double p0[4 * N], p1[4 * N];
-        const double w0 = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r0, p0);
-        const double w1 = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r1, p1);
+        const double w0 = gen_event<N, MODE>(a.d, tb, h, a.rp, a.ev_begin + (uint64_t)r0, p0);
+        const double w1 = gen_event<N, MODE>(a.d, tb, h, a.rp, a.ev_begin + (uint64_t)r1, p1);
         if (a.store) {
           if constexpr (VEC2) {
             __stcs(reinterpret_cast<double2*>(a.cols[0] + r0), make_double2(w0, w1));
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
       const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
       if (r < a.count) {
         double p[4 * N];
-        const double w = gen_event<N, MODE>(a.d, tb, a.rp, a.ev_begin + (uint64_t)r, p);
+        const double w = gen_event<N, MODE>(a.d, tb, h, a.rp, a.ev_begin + (uint64_t)r, p);
         if (a.d.moving) {
 #pragma unroll
           for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
@@ -314,11 +315,11 @@ __device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a, in
 // parent), so its four-vector is a register reference instead of a select chain.
 template <int N, int NS, int MODE, int K>
 __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, const TwoBody& tb,
-                                            int64_t r, unsigned long long* bad) {
+                                            const RestHoist& hp, int64_t r, unsigned long long* bad) {
   const int k = K >= 0 ? K : a.k;
   const uint64_t row = a.ev_begin + (uint64_t)r;
   double p[4 * N];
-  const double wp = rest_event<N, MODE>(a.d, a.rp, row, p);
+  const double wp = rest_event<N, MODE>(a.d, a.rp, row, p, hp);
   if (a.d.moving) {
 #pragma unroll
     for (int j = 0; j < N; ++j) boost_fma(mf, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
@@ -381,14 +382,15 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
   unsigned long long bad = ~0ull;
   TwoBody tb{};
   if constexpr (NS == 2) tb = two_body_consts(a.sub);
+  const RestHoist hp = rest_hoist<N>(a.d);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     double acc[2] = {0.0, 0.0};
     if (HK_CHAIN_ILP == 2 && N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
         const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
-        const double w0 = chain_row<N, NS, MODE, K>(a, mf, tb, r0, &bad);
-        const double w1 = chain_row<N, NS, MODE, K>(a, mf, tb, r0 + HK_CHUNK / 2, &bad);
+        const double w0 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0, &bad);
+        const double w1 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0 + HK_CHUNK / 2, &bad);
         acc[0] += w0;
         acc[1] += w0 * w0;
         acc[0] += w1;
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
       for (int i = 0; i < kRowsPerThread; ++i) {
         const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
         if (r < a.count) {
-          const double w = chain_row<N, NS, MODE, K>(a, mf, tb, r, &bad);
+          const double w = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r, &bad);
           acc[0] += w;
           acc[1] += w * w;
         }
