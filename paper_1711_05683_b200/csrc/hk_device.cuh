@@ -385,6 +385,8 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
   double w = 1.0;
 #pragma unroll
   for (int k = 1; k < N; ++k) {
+    // (hoisting the decay-fixed products too -- inv0^2, 4 inv0^2 m1^2, M_last^2
+    // -- measured no faster: 1.969 ms either way; ptxas already keeps them)
     ps[k] = k == N - 1 ? pstar_r(inv[k], inv[k - 1], d.masses[k] * d.masses[k], h.rcp_2m_last)
                        : pstar(inv[k], inv[k - 1], d.masses[k] * d.masses[k]);
     w = w * ps[k];
