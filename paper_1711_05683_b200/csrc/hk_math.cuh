@@ -1,17 +1,13 @@
-// hk_math.cuh -- our own fp64 sin/cos(pi t) and exp, kept as measured
-// alternatives to libdevice's (which the kernels use by default).
+// hk_math.cuh -- our own fp64 sin/cos(pi t) and exp.
 //
-// Motivation: libdevice materialises each polynomial coefficient as a 64-bit
-// immediate (two UMOVs per coefficient per call; sincospi ~75 issued
-// instructions, 24 of them UMOV).  Measured on B200:
-//   - coefficients from the constant bank (HK_MATH_CONST_BANK): slower
-//     (generator +2.6%, FCN +27%);
-//   - coefficients as immediates: sincospi ties libdevice (2.315 vs 2.305 ms
-//     per 1e8 events), exp is slower than libdevice's in the FCN (45.6 vs
-//     35.8 us).
-// So k_sincospi/k_exp default to libdevice; -DHK_MATH_OWN_SINCOSPI /
-// -DHK_MATH_OWN_EXP select these.  The functions are __host__ __device__ so
-// tests/test_math_host.py checks them against long double on the CPU.
+// The generator uses sincospi_gen (near-minimax, ~30 instructions; libdevice's
+// sincospi takes 53 on sm_100a); k_exp defaults to libdevice's exp, which
+// measured faster in the FCN (35.8 vs 45.6 us for ours).  Earlier
+// measurements on B200: coefficients from the constant
+// bank (HK_MATH_CONST_BANK) were slower (generator +2.6%, FCN +27%); the
+// Taylor-form sincospi below tied libdevice (2.315 vs 2.305 ms per 1e8).
+// The functions are __host__ __device__ so tests/test_math_host.py checks
+// them against long double on the CPU.
 //
 // Accuracy (CPU, 2^22 points):
 //   sincospi: |error| <= 2 ulp(1) absolute for |t| < 2^20
@@ -135,8 +131,15 @@ HK_HD void sincospi_gen(double t, double* s, double* c) {
   const int iq = (int)q;
   double sn = (iq & 1) ? pc : sr;
   double cs = (iq & 1) ? sr : pc;
+#if defined(__CUDA_ARCH__)
+  // quadrant signs as sign-bit flips on the high word (exact, like negation)
+  sn = __hiloint2double(__double2hiint(sn) ^ (int)(((unsigned)iq & 2u) << 30), __double2loint(sn));
+  cs = __hiloint2double(__double2hiint(cs) ^ (int)(((unsigned)(iq + 1) & 2u) << 30),
+                        __double2loint(cs));
+#else
   sn = (iq & 2) ? -sn : sn;
   cs = ((iq + 1) & 2) ? -cs : cs;
+#endif
   *s = sn;
   *c = cs;
 }
