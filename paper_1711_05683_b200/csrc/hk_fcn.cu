@@ -109,6 +109,14 @@ struct LogProd {
     m *= __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
   }
 
+  // add() for a value known to be a normal double (the factored density's s):
+  // no subnormal check, same result
+  __device__ __forceinline__ void add_normal(double d) {
+    const long long b = __double_as_longlong(d);
+    e += (int)((b >> 52) & 0x7ff) - 1023;
+    m *= __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+  }
+
   // move m's binary exponent into e (exact): keeps m in [1, 2) so a thread
   // can multiply any number of events with one log at the end
   __device__ __forceinline__ void renorm() {
@@ -139,7 +147,7 @@ __device__ __forceinline__ void fcn_row(const Coeffs& c, double xv, int64_t row,
   if (V == kFcnFactored) {
     double s, M;
     if (density_factored(c, xv, &s, &M)) {
-      lp.add(s);
+      lp.add_normal(s);  // s in [min amp, amp0 + amp1]: normal
       msum += M;
       return;
     }
