@@ -82,6 +82,8 @@ __device__ __forceinline__ bool density_factored(const Coeffs& c, double x, doub
   const double z = (x - c.shift[0]) * c.scale[0];
   const double A = -0.5 * z * z;
   const double B = x * c.scale[1];
+  // (fmax(A, B) and exp(-|A - B|) instead of the selects measured slower:
+  // 29.8 vs 29.0 us per 1e7 events)
   const bool ga = A >= B;  // NaN: false, M = B = NaN
   *M = ga ? A : B;
   const double t = fcn_exp(ga ? B - A : A - B);
