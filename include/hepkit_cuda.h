@@ -136,6 +136,43 @@ int hk_device_info(int* n_devices, int* sm_count);
 /* Number of 4096-row chunk partials for ev_count rows. */
 int64_t hk_num_chunks(int64_t ev_count);
 
+/* ------------------------------------------------- lifetime + collectives
+ * For a C host that drives several GPUs from ONE process -- the analogue of
+ * the reference's `workers` pool (parallel.py:18-92), with devices in place
+ * of processes.  The Python drop-in does not use these: it runs one process
+ * per GPU and exchanges the same partials with torch.distributed (parallel.py
+ * in this package).  NCCL (libnccl.so.2) is dlopen'ed by hk_init, so the
+ * library has no link-time NCCL dependency.
+ *
+ * hk_init(n): one NCCL communicator per device 0..n-1 (ncclCommInitAll), a
+ * clique the two collectives below run over; n = 1 is valid (a one-rank
+ * clique).  HK_EINVAL when n exceeds the visible devices, HK_ECUDA when NCCL
+ * is unavailable.  Calling it again with another n rebuilds the clique.
+ * hk_shutdown(): destroys the clique and releases the library's cached state
+ * (NVRTC-specialised modules, this thread's mapped FCN mailboxes and copy
+ * streams).  The library stays usable; those caches rebuild on demand. */
+int hk_init(int32_t n_devices);
+int hk_shutdown(void);
+/* Devices in the current clique (0 before hk_init / after hk_shutdown). */
+int32_t hk_clique_size(void);
+
+/* In-place sum of `count` doubles across the clique: d_bufs[g] lives on
+ * device g, streams[g] is device g's stream (NULL = legacy default).  Returns
+ * after the work is enqueued (stream-ordered, like a kernel launch).  A sum
+ * over devices is deterministic for a fixed clique size but not invariant to
+ * it; use hk_allgather_partials + hk_fold_partials for bitwise device-count
+ * invariance (SURVEY.md 8(e) option ii). */
+int hk_allreduce_partials(double* const* d_bufs, int32_t n_dev, int64_t count,
+                          void* const* streams);
+/* Every device receives all devices' partials in device order:
+ * d_recv[g][h * count + i] = d_send[h][i].  d_recv[g] holds n_dev * count
+ * doubles.  When the devices hold consecutive, equal-length runs of chunk
+ * partials (shards split on HK_CHUNK boundaries), folding d_recv[g] in order
+ * (hk_fold_partials) gives every device the same total, bit-identical to the
+ * one-device fold of the whole chunk sequence. */
+int hk_allgather_partials(const double* const* d_send, double* const* d_recv, int32_t n_dev,
+                          int64_t count, void* const* streams);
+
 /* -------------------------------------------------------------------- RNG */
 /* rng.py:115-120 raw64 / :123-125 uniform_array at key.counter + d_counters[i].
  * Mode HK_RNG_PHILOX is not a reference stream (uniform only, for tests). */

@@ -42,6 +42,7 @@ EXPORTS = (
     "hk_sample_pdf", "hk_unweight_flags", "hk_compact", "hk_scan_counts",
     "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
     "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles", "hk_fold_segments",
+    "hk_init", "hk_shutdown", "hk_clique_size", "hk_allreduce_partials", "hk_allgather_partials",
 )
 
 
@@ -134,6 +135,11 @@ _SIGS = {
     "hk_nll_work_doubles": (_I64, [_I64]),
     "hk_fold_segments": (_INT, [_P, _I64, _I32, _I32, _P, _P]),
     "hk_format_csv": (_INT, [_PP, _I32, _I64, _P, _P, _I64, ctypes.POINTER(_I64), _P]),
+    "hk_init": (_INT, [_I32]),
+    "hk_shutdown": (_INT, []),
+    "hk_clique_size": (_I32, []),
+    "hk_allreduce_partials": (_INT, [_PP, _I32, _I64, _PP]),
+    "hk_allgather_partials": (_INT, [_PP, _PP, _I32, _I64, _PP]),
 }
 
 _lock = threading.Lock()
@@ -383,3 +389,51 @@ def jit_compile(program, n_daughters: int = 0, rng_mode: int = HK_RNG_REFERENCE)
     check(load_library().hk_jit_compile(program, n_daughters, rng_mode, ctypes.byref(out)),
           "hk_jit_compile")
     return out.value
+
+
+# ---------------------------------------------------- lifetime + collectives
+# For one process driving GPUs 0..n-1 (a C host's view of the reference's
+# worker pool).  The drop-in API itself runs one process per GPU and uses
+# torch.distributed (parallel.py); these are the C-ABI equivalents.
+
+def init(n_devices: int = 1) -> None:
+    """hk_init: NCCL clique over devices 0..n_devices-1 (NCCL dlopen'ed)."""
+    check(load_library().hk_init(int(n_devices)), "hk_init")
+
+
+def shutdown() -> None:
+    """hk_shutdown: destroy the clique and release cached modules/buffers."""
+    check(load_library().hk_shutdown(), "hk_shutdown")
+
+
+def clique_size() -> int:
+    return int(load_library().hk_clique_size())
+
+
+def _clique_args(tensors):
+    t = torch()
+    n = tensors[0].numel()
+    for g, x in enumerate(tensors):
+        if x.dtype != t.float64 or not x.is_contiguous() or x.numel() != n:
+            raise ValueError("partials must be contiguous fp64 tensors of equal length")
+        if x.device.type != "cuda" or x.device.index != g:
+            raise ValueError(f"partials[{g}] must live on cuda:{g}, found {x.device}")
+    streams = (ctypes.c_void_p * len(tensors))(
+        *[t.cuda.current_stream(x.device).cuda_stream for x in tensors])
+    return n, streams
+
+
+def allreduce_partials(bufs) -> None:
+    """In-place sum across the clique (hk_allreduce_partials); bufs[g] on cuda:g."""
+    n, streams = _clique_args(bufs)
+    check(lib().hk_allreduce_partials(ptr_array(bufs), len(bufs), n, streams), "hk_allreduce_partials")
+
+
+def allgather_partials(sends) -> list:
+    """Every device gets all devices' partials in device order (hk_allgather_partials)."""
+    n, streams = _clique_args(sends)
+    t = torch()
+    recv = [t.empty(len(sends) * n, dtype=t.float64, device=x.device) for x in sends]
+    check(lib().hk_allgather_partials(ptr_array(sends), ptr_array(recv), len(sends), n, streams),
+          "hk_allgather_partials")
+    return recv

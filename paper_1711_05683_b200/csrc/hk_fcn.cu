@@ -486,11 +486,12 @@ struct Mailbox {
   int device = -1;
 };
 
+thread_local Mailbox t_boxes[16];
+
 int mailbox(Mailbox** out) {
-  thread_local Mailbox boxes[16];
   int dev = 0;
   HK_CUDA(cudaGetDevice(&dev));
-  Mailbox& m = boxes[dev & 15];
+  Mailbox& m = t_boxes[dev & 15];
   if (m.device != dev) {
     void* p = nullptr;
     HK_CUDA(cudaHostAlloc(&p, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
@@ -504,6 +505,15 @@ int mailbox(Mailbox** out) {
   }
   *out = &m;
   return HK_OK;
+}
+
+// hk_shutdown: free this thread's mailboxes (rebuilt by the next hk_nll_eval)
+void fcn_release() {
+  for (Mailbox& m : t_boxes) {
+    if (m.device < 0) continue;
+    cudaFreeHost(const_cast<unsigned long long*>(m.h));
+    m = Mailbox{};
+  }
 }
 
 // Tile schedule of the one-launch FCN: plain 4096-row tiles.  The spread-tail

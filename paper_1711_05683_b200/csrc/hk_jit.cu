@@ -400,6 +400,14 @@ int jit_integrate(const hk_program_t& P, int n, int mode, int64_t rows, const vo
   return lookup(P, n, mode, rows, 0, fn);
 }
 
+// hk_shutdown: unload every specialised module (no launch may be in flight)
+void jit_release() {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& kv : g_cache)
+    if (kv.second.lib) cudaLibraryUnload(kv.second.lib);
+  g_cache.clear();
+}
+
 }  // namespace hk
 
 using namespace hk;

@@ -40,11 +40,12 @@ struct CopyLane {
   cudaEvent_t freed[2] = {nullptr, nullptr};
 };
 
+thread_local CopyLane t_lanes[16];
+
 int copy_lane(CopyLane** out) {
-  static thread_local CopyLane lanes[16];
   int dev = 0;
   HK_CUDA(cudaGetDevice(&dev));
-  CopyLane& L = lanes[dev & 15];
+  CopyLane& L = t_lanes[dev & 15];
   if (L.device != dev) {
     HK_CUDA(cudaStreamCreateWithFlags(&L.copy, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
@@ -55,6 +56,23 @@ int copy_lane(CopyLane** out) {
   }
   *out = &L;
   return HK_OK;
+}
+
+// hk_shutdown: destroy this thread's copy streams/events (rebuilt on demand)
+void copy_lane_release() {
+  for (CopyLane& L : t_lanes) {
+    if (L.device < 0) continue;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(L.device);
+    cudaStreamDestroy(L.copy);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(L.made[b]);
+      cudaEventDestroy(L.freed[b]);
+    }
+    cudaSetDevice(cur);
+    L = CopyLane{};
+  }
 }
 
 }  // namespace hk

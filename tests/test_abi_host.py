@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_functions() -> set[str]:
     text = open(os.path.join(ROOT, "include", "hepkit_cuda.h")).read()
-    return set(re.findall(r"^(?:int|int64_t)\s+(hk_\w+)\(", text, flags=re.M))
+    return set(re.findall(r"^(?:int|int32_t|int64_t)\s+(hk_\w+)\(", text, flags=re.M))
 
 
 def test_library_exports_every_declared_symbol(hk):
@@ -93,6 +93,27 @@ def test_every_entry_point_marshals_and_validates(hk):
     nd, sm = ctypes.c_int(-1), ctypes.c_int(-1)
     assert L.hk_device_info(ctypes.byref(nd), ctypes.byref(sm)) == OK
     assert nd.value >= 0
+
+
+def test_clique_lifetime_validation(hk):
+    """hk_init / hk_shutdown / the clique collectives: argument and state
+    checks run on the host (no device, no NCCL needed)."""
+    import torch
+    from paper_1711_05683_b200 import _lib
+    L = _lib.load_library()
+    bufs = (ctypes.c_void_p * 1)(1)
+    if not torch.cuda.is_available():
+        assert L.hk_init(1) == _lib.HK_EINVAL
+        assert "visible" in _lib.last_error()
+        with pytest.raises(ValueError):
+            _lib.init(1)
+    assert L.hk_init(0) == _lib.HK_EINVAL
+    assert L.hk_shutdown() == _lib.HK_OK      # idempotent, nothing to release
+    assert L.hk_clique_size() == 0
+    assert L.hk_allreduce_partials(bufs, 1, 4, None) == _lib.HK_EINVAL
+    assert "hk_init" in _lib.last_error()
+    assert L.hk_allgather_partials(bufs, bufs, 1, 4, None) == _lib.HK_EINVAL
+    assert "hk_init" in _lib.last_error()
 
 
 def test_struct_layouts_match_header(hk):
