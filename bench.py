@@ -54,6 +54,26 @@ def _traffic() -> float | None:
         return None
 
 
+def _fp64_roofline(kernel: str, events_per_s_per_gpu: float, note: str = "") -> dict | None:
+    """FP64-pipe roofline of an FP64-bound kernel (C4 FCN, C5 fused integration;
+    SURVEY.md 8(d)): the live per-GPU event rate x the kernel's DP instructions
+    per event (ncu, committed) against the DFMA instruction rate measured by
+    tools/fp64_peak.cu (committed; MEASURED_PEAKS.json has no FP64 figure)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_roofline.json")) as fh:
+            d = json.load(fh)
+        k, pk = d["kernels"][kernel], d["peak"]
+    except (OSError, KeyError, ValueError):
+        return None
+    inst = events_per_s_per_gpu * k["dp_inst_per_event"]
+    return {"bound": "fp64", "kernel": k["kernel"], "achieved": inst * 1e-12, "peak": pk["dp_inst_per_s"] * 1e-12,
+            "unit": "T DP inst/s", "frac": inst / pk["dp_inst_per_s"],
+            "tflops": events_per_s_per_gpu * k["dp_flops_per_event"] * 1e-12, "peak_tflops": pk["tflops"],
+            "dp_inst_per_event": k["dp_inst_per_event"],
+            "source": "per-event DP counts: profiles/r01_fp64_roofline.json (ncu); peak: " + pk["source"],
+            **({"note": note} if note else {})}
+
+
 class NvmlClockSampler:
     """SM clock + clock-event reasons polled through NVML every ~0.5 ms in a
     thread for exactly the timed region (the region is tens of ms, shorter
@@ -290,6 +310,10 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
             "unit": "evals/s", "n_gpus": world, "scaling": "strong", "us_per_eval": dt * 1e6,
             "kernel_us_per_eval": kt * 1e6, "c_abi_us_per_eval": ct * 1e6,
             "kernel_events_per_s": FCN_EVENTS / kt, "evals": evals,
+            "roofline": _fp64_roofline("k_nll_fused", n_local / kt,
+                                       "rate from kernel_us_per_eval (k_nll<factored>, back to back); DP counts "
+                                       "of the API's k_nll_fused<2>, the same per-event arithmetic plus the "
+                                       "last-CTA fold"),
             "timing": "CUDA events around the eval loop on each rank's stream (each eval ends with the value "
                       "on the host), max over ranks",
             "parallelism": f"row shards of {n_local} events per GPU, rank-order fold of per-rank log-sums",
@@ -412,7 +436,8 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     mu = tot[1] / tot[0]
     out["C5"] = {"workload": "1e10 B0->J/psi K pi events, fused generation + <m12^2> weighted average, "
                              f"strong scaling over {world} GPU(s), no event store",
-                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu)}
+                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu),
+                 "roofline": _fp64_roofline("hk_jit_integrate", n5 / dt / world)}
     # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
     # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
     expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
