@@ -438,6 +438,26 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
                              f"strong scaling over {world} GPU(s), no event store",
                  "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu),
                  "roofline": _fp64_roofline("hk_jit_integrate", n5 / dt / world)}
+    # C5 secondary integrand: K*(892) Breit-Wigner on m^2_K pi, the named builtin
+
+    def m23(cols):
+        e = cols["p2_e"] + cols["p3_e"]
+        px = cols["p2_px"] + cols["p3_px"]
+        py = cols["p2_py"] + cols["p3_py"]
+        pz = cols["p2_pz"] + cols["p3_pz"]
+        return (e * e - px * px - py * py - pz * pz,)
+
+    def c5bw():
+        parts = hk.phsp_integrate(hk.breit_wigner(0.89555, 0.0473), spec, mother, b - a, hk.RngKey(1, 1), m23,
+                                  row_offset=a, return_partials=True)
+        full = gather_partials(parts, n5, 5)
+        res["tot"] = _lib.fold(full, _lib.num_chunks(n5), 5)
+
+    dt = _timed(torch, c5bw, 2, dist)
+    tot = res["tot"].cpu().numpy()
+    out["C5_bw"] = {"workload": "1e10 events, fused generation + <BW_K*(892)(m^2_K pi)> (M=0.89555, G=0.0473), "
+                                f"strong scaling over {world} GPU(s), no event store",
+                    "value": n5 / dt, "unit": "events/s", "seconds": dt, "bw_average": float(tot[1] / tot[0])}
     # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
     # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
     expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
