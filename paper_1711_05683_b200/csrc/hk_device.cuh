@@ -363,12 +363,11 @@ __device__ __forceinline__ RestHoist rest_hoist(const hk_decay_t& d) {
   return h;
 }
 
-template <int N, int MODE>
-__device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParams& rp,
-                                             uint64_t row, double (&p)[4 * N], const RestHoist& h) {
-  constexpr int D = 3 * N - 4;  // phasespace.py:84-86
-  uint64_t bits[D];
-  draw_bits<D, MODE>(rp, row, bits);
+// The event from its D = 3N - 4 drawn uniforms (as 53-bit integers); split from
+// the draw so a kernel can draw the next rows while this one computes.
+template <int N>
+__device__ __forceinline__ double rest_event_bits(const hk_decay_t& d, uint64_t (&bits)[3 * N - 4],
+                                                  double (&p)[4 * N], const RestHoist& h) {
   // sorted mass uniforms: odd-even transposition network, integer compares
 #pragma unroll
   for (int pass = 0; pass < N - 2; ++pass) {
@@ -422,6 +421,14 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
     p[4 * k + 3] = -clz;
   }
   return w;
+}
+
+template <int N, int MODE>
+__device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParams& rp,
+                                             uint64_t row, double (&p)[4 * N], const RestHoist& h) {
+  uint64_t bits[3 * N - 4];  // phasespace.py:84-86
+  draw_bits<3 * N - 4, MODE>(rp, row, bits);
+  return rest_event_bits<N>(d, bits, p, h);
 }
 
 template <int N, int MODE>
