@@ -269,6 +269,58 @@ def test_survey_appendix_1e6_values(cuda, hk):
     assert wm.sum_w == pytest.approx(616817.9666723448, rel=1e-10)
 
 
+def test_c5_full_size_chunk_partials(cuda, hk, oracle):
+    """Config C5 at full size (1e10 events, fused, nothing stored) in one
+    launch.  Size-independent properties: each 4096-row chunk's five moments
+    depend only on that chunk's rows, so windows regenerated at far offsets
+    give bit-identical partials -- including the ragged last chunk (1e10 is
+    not a multiple of 4096) -- and match the oracle's chunk sums there."""
+    spec, mother = _b0(hk)
+    n = 10_000_000_000
+    parts = hk.phsp_integrate(hk.identity(), spec, mother, n, hk.RngKey(1, 1), m12sq_builder,
+                              return_partials=True)
+    n_chunks = (n + 4095) // 4096
+    assert parts.numel() == 5 * n_chunks
+    for c0 in (0, 1_234_567, 2_000_000, n_chunks - 7):
+        s = c0 * 4096
+        m = min(7 * 4096, n - s)
+        win = hk.phsp_integrate(hk.identity(), spec, mother, m, hk.RngKey(1, 1), m12sq_builder,
+                                row_offset=s, return_partials=True)
+        k = win.numel() // 5
+        assert cuda.equal(win, parts[5 * c0:5 * (c0 + k)]), f"chunks {c0}..{c0 + k}"
+        ref = oracle.generate(B0_DAUGHTERS, B0_MASS, m, 1, 1, ev_begin=s, threads=4)
+        f = oracle.pair_mass2(ref, 1, 2) + 0.0
+        got = win.view(k, 5).cpu().numpy()
+        for j, (a, b) in enumerate(oracle.chunk_windows(m)):
+            want = oracle.average(ref["weight"][a:b], f[a:b])[2]
+            np.testing.assert_allclose(got[j], want, rtol=1e-12, err_msg=f"chunk {c0 + j}")
+    tot = parts.view(n_chunks, 5).sum(0).cpu().numpy()
+    mu = tot[1] / tot[0]
+    assert mu == pytest.approx(18.920064852245346, rel=2e-4)   # the 1e6-event value, within MC error
+
+
+def test_c3_full_size_chain_windows(cuda, hk, oracle):
+    """Config C3's per-GPU shard (1.25e8 chained events = 1e9 / 8, 17 columns,
+    17 GB) in one fused launch.  Windows at far offsets are regenerated by the
+    oracle's generate + decay_chain, and four-momentum conservation holds over
+    the whole block."""
+    spec, mother = _b0(hk)
+    sub = hk.DecaySpec(M_JPSI, (M_MU, M_MU))
+    n = 125_000_000
+    ch = hk.phsp_generate_chain(spec, mother, n, hk.RngKey(1, 1), 1, sub, hk.RngKey(2, 1))
+    assert len(ch) == n
+    for s in (0, 4096 * 12_345 + 17, 99_999_999, n - 1000):
+        par = oracle.generate(B0_DAUGHTERS, B0_MASS, 1000, 1, 1, ev_begin=s)
+        ref = oracle.decay_chain(par, 1, (M_MU, M_MU), M_JPSI, 2, 1, ev_begin=s)
+        got = np.stack([ch.device_column(c)[s:s + 1000].cpu().numpy() for c in ch.schema.names])
+        assert_block_parity(got, np.stack(list(ref.values())), 4, f"C3 window {s}")
+    torch = cuda
+    for c, target in (("e", B0_MASS), ("px", 0.0), ("py", 0.0), ("pz", 0.0)):
+        tot = sum(ch.device_column(f"p{k}_{c}") for k in (1, 2, 3, 4))
+        assert float(torch.max(torch.abs(tot - target))) <= 1e-9 * B0_MASS, c
+    del ch
+
+
 def test_average_errors(cuda, hk):
     spec, mother = _b0(hk)
     blk = hk.phsp_generate(spec, mother, 70_000, hk.RngKey(3, 1))
