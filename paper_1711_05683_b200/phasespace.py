@@ -23,6 +23,7 @@ from __future__ import annotations
 import ctypes
 import functools
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -143,17 +144,19 @@ def phsp_generate_to_host(spec: DecaySpec, mother: FourVector, n_events: int, ke
         out = [torch.empty(n_events, dtype=torch.float64, pin_memory=True) for _ in range(ncols)]
     head = (2 * _lib.num_weight_slices(n_events) + 2 * _lib.num_chunks(n_events) + 2) * 8
     stage_bytes = max(int(stage_bytes), head + 2 * ncols * 8 * _lib.HK_CHUNK)
-    stage = _stage_buffer(stage_bytes)
     sums = (ctypes.c_double * 2)()
-    _lib.check(_lib.lib().hk_phsp_generate_host(d, k, _lib.u64(row_offset), int(n_events),
-                                                _lib.ptr_array(out), sums, _lib.ptr(stage),
-                                                stage.numel(), _lib.stream_ptr()),
-               "hk_phsp_generate_host")
+    with _stage_lock:                     # one staging buffer per device, one user at a time
+        stage = _stage_buffer(stage_bytes)
+        _lib.check(_lib.lib().hk_phsp_generate_host(d, k, _lib.u64(row_offset), int(n_events),
+                                                    _lib.ptr_array(out), sums, _lib.ptr(stage),
+                                                    stage.numel(), _lib.stream_ptr()),
+                   "hk_phsp_generate_host")
     store = ColumnStore.from_columns(phsp_schema(spec.n), [t.numpy() for t in out])
     return store, (sums[0], sums[1])
 
 
 _stage_cache: dict = {}
+_stage_lock = threading.Lock()
 
 
 def _stage_buffer(nbytes: int):
