@@ -199,10 +199,13 @@ __device__ __forceinline__ double fast_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   // x = 0: the seed is +inf; clamping it makes every step below exact zeros
-  // (0 * 1e300 = 0), so sqrt(0) = 0 without a compare-and-select; NaN seeds
-  // clamp to 1e300 too and x * y keeps the NaN.  Positive normal x (seed
-  // < 2e153) are untouched.
-  y = fmin(y, 1e300);
+  // (0 * ~1e300 = 0), so sqrt(0) = 0 without a compare-and-select.  The clamp
+  // is one integer min on the seed's high word (positive doubles order like
+  // their high words; +inf 0x7ff00000 -> 0x7e37e43c ~ 1e300), not fmin's
+  // DSETP + 2 FSEL on the contended FP64 pipe.  NaN seeds (x NaN: sign set,
+  // negative as int) pass unchanged and x * y keeps the NaN; positive normal
+  // x (seed < 2e153, high word < 0x5fd00000) are untouched.
+  y = __hiloint2double(min(__double2hiint(y), 0x7e37e43c), __double2loint(y));
   double s = x * y;  // sqrt(x), seed accuracy
   double h = 0.5 * y;  // 1 / (2 sqrt(x))
   const double r = fma(-s, h, 0.5);  // one coupled Goldschmidt step
@@ -231,12 +234,13 @@ __device__ __forceinline__ Frame make_frame_fast(double fe, double fx, double fy
   return f;
 }
 
-// make_frame_fast with fast_rcp(fm) supplied (a frame whose mass is fixed)
+// make_frame_fast for a frame whose mass is fixed by the decay: gmul is
+// fast_rcp(fm), or +inf for fm == +0 (fe * inf is IEEE fe / +0), selected
+// once per launch instead of per event
 __device__ __forceinline__ Frame make_frame_fast_r(double fe, double fx, double fy, double fz,
-                                                   double fm, double rcp_fm) {
+                                                   double gmul) {
   Frame f;
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  f.gamma = fm == 0.0 ? fe * inf : fe * rcp_fm;
+  f.gamma = fe * gmul;
   const double r = fast_rcp(fe);
   f.bx = fx * r;
   f.by = fy * r;
@@ -275,6 +279,10 @@ __device__ __forceinline__ void boost_rest(const Frame& f, double m, double& e, 
 __device__ __forceinline__ double cr_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  // x = +0: the +inf seed clamps to ~1e300 (integer min on the high word, as
+  // in fast_sqrt), so every step below is an exact zero and sqrt(+0) = +0;
+  // positive normal x (seed high word < 0x5fd00000) are untouched
+  y = __hiloint2double(min(__double2hiint(y), 0x7e37e43c), __double2loint(y));
   double t = x * y;
   y = fma(0.5 * y, fma(-t, y, 1.0), y);
   t = x * y;
@@ -297,9 +305,14 @@ __device__ __forceinline__ double cr_div(double a, double b) {
 // lam > 0, 0 for lam <= 0, NaN propagated.  lam = t*t - (4 a2) b2 of GeV-scale
 // squares is either 0 or >= ~1e-20 (a multiple of ulp(t*t)), never subnormal,
 // so cr_sqrt's normal-range domain covers it.
+// np.maximum(lam, 0) as integer ops (no FP64-pipe compares): a set sign bit
+// clears both words, so negative lam and -0 become +0 and cr_sqrt gives +0.
+// NaN propagates: the FP64 units only produce the positive canonical NaN, and
+// lam is formed by subtraction (no negation that could set a NaN's sign).
 __device__ __forceinline__ double sqrt_lambda(double lam) {
-  const double s = cr_sqrt(lam);
-  return lam > 0.0 ? s : (lam == lam ? 0.0 : lam);
+  const int hi = __double2hiint(lam);
+  const int keep = ~(hi >> 31);  // all ones unless the sign bit is set
+  return cr_sqrt(__hiloint2double(hi & keep, __double2loint(lam) & keep));
 }
 
 // Two-body breakup momentum (phasespace.py:67-71), reference op order; b2 = m*m
@@ -349,17 +362,18 @@ __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
 // Per-decay reciprocals of rest_event<N>, hoistable out of the event loop
 // (computed with the very operations rest_event would use, so events are
 // bit-identical): 1/(2M) of the last breakup (M = inv[N-1] is fixed by the
-// decay) and 1/inv[0] of the first cluster frame.
+// decay) and the first cluster frame's gamma multiplier: 1/inv[0], or +inf
+// when inv[0] = m1 = 0 (so fe * gmul0 is IEEE fe / +0).
 struct RestHoist {
   double rcp_2m_last;
-  double rcp_inv0;
+  double gmul0;  // make_frame_fast_r's gamma multiplier of the first cluster frame
 };
 
 template <int N>
 __device__ __forceinline__ RestHoist rest_hoist(const hk_decay_t& d) {
   RestHoist h;
   h.rcp_2m_last = fast_rcp(2.0 * (d.T + d.csum[N - 1]));
-  h.rcp_inv0 = fast_rcp(d.csum[0]);
+  h.gmul0 = d.csum[0] == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : fast_rcp(d.csum[0]);
   return h;
 }
 
@@ -407,7 +421,7 @@ __device__ __forceinline__ double rest_event_bits(const hk_decay_t& d, uint64_t 
     const double clm = inv[k - 1];
     const double cle = fast_sqrt(q * q + clm * clm);
     const double clx = q * nx, cly = q * ny, clz = q * nz;
-    const Frame f = k == 1 ? make_frame_fast_r(cle, clx, cly, clz, clm, h.rcp_inv0)
+    const Frame f = k == 1 ? make_frame_fast_r(cle, clx, cly, clz, h.gmul0)
                            : make_frame_fast(cle, clx, cly, clz, clm);
     if (k == 1) {
       boost_rest(f, d.masses[0], p[0], p[1], p[2], p[3]);  // daughter 1 starts at rest
