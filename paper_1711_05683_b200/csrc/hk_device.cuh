@@ -195,17 +195,27 @@ __device__ __forceinline__ double fast_rcp(double x) {
 // (< 2.2e-308 GeV^2, physically impossible here) would also pass through.
 // Used for energies and |sin theta|, never for the breakup momenta that
 // make up the weight.
+// The f64 rsqrt seed (MUFU.RSQ64H: a ~1e-6 accurate high word, low word 0),
+// clamped to <= ~1e300 by one integer min on the high word: positive doubles
+// order like their high words, so +inf (x = +0) becomes ~1e300, NaN seeds
+// (sign set, negative as int) pass unchanged and positive normal x (seed high
+// word < 0x5fd00000) are untouched.  The low word is the raw high word
+// instead of 0: a <= 2^-20 relative perturbation of a 1e-6 seed, gone after
+// the refinement steps (results bit-identical), and it saves the move that
+// zeroes the low register of every seed.
+__device__ __forceinline__ double rsqrt_seed_clamp(double y) {
+  const int hi = __double2hiint(y);
+  return __hiloint2double(min(hi, 0x7e37e43c), hi);
+}
+
 __device__ __forceinline__ double fast_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   // x = 0: the seed is +inf; clamping it makes every step below exact zeros
-  // (0 * ~1e300 = 0), so sqrt(0) = 0 without a compare-and-select.  The clamp
-  // is one integer min on the seed's high word (positive doubles order like
-  // their high words; +inf 0x7ff00000 -> 0x7e37e43c ~ 1e300), not fmin's
-  // DSETP + 2 FSEL on the contended FP64 pipe.  NaN seeds (x NaN: sign set,
-  // negative as int) pass unchanged and x * y keeps the NaN; positive normal
-  // x (seed < 2e153, high word < 0x5fd00000) are untouched.
-  y = __hiloint2double(min(__double2hiint(y), 0x7e37e43c), __double2loint(y));
+  // (0 * ~1e300 = 0), so sqrt(0) = 0 without a compare-and-select -- and
+  // without fmin's DSETP + 2 FSEL on the contended FP64 pipe.  A NaN x keeps
+  // its NaN through x * y.
+  y = rsqrt_seed_clamp(y);
   double s = x * y;  // sqrt(x), seed accuracy
   double h = 0.5 * y;  // 1 / (2 sqrt(x))
   const double r = fma(-s, h, 0.5);  // one coupled Goldschmidt step
@@ -279,10 +289,9 @@ __device__ __forceinline__ void boost_rest(const Frame& f, double m, double& e, 
 __device__ __forceinline__ double cr_sqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  // x = +0: the +inf seed clamps to ~1e300 (integer min on the high word, as
-  // in fast_sqrt), so every step below is an exact zero and sqrt(+0) = +0;
-  // positive normal x (seed high word < 0x5fd00000) are untouched
-  y = __hiloint2double(min(__double2hiint(y), 0x7e37e43c), __double2loint(y));
+  // x = +0: the +inf seed clamps to ~1e300 (as in fast_sqrt), so every step
+  // below is an exact zero and sqrt(+0) = +0
+  y = rsqrt_seed_clamp(y);
   double t = x * y;
   y = fma(0.5 * y, fma(-t, y, 1.0), y);
   t = x * y;
