@@ -238,6 +238,14 @@ __device__ __forceinline__ double frame_mass(double fe, double fx, double fy, do
   return m2 > 1e-300 && m2 < 1e300 ? cr_sqrt(m2) : sqrt(max0(m2));
 }
 
+// frame_mass for a daughter this kernel generated itself (fused chain): its
+// m2 is finite, below M^2 < 1e300, and either >= ~ulp(GeV^2) or <= 0, so
+// sqrt_lambda's sign mask + cr_sqrt (sqrt(+0) = +0) is the same correctly
+// rounded value with no FP64 compares and no slow-path branch.
+__device__ __forceinline__ double gen_frame_mass(double fe, double fx, double fy, double fz) {
+  return sqrt_lambda(fe * fe - fx * fx - fy * fy - fz * fz);
+}
+
 __device__ __forceinline__ bool mass_mismatch(double fm, double M) {
   const double tol = 1e-9 * (M > 1e-6 ? M : 1e-6);  // MASS_TOLERANCE * max(M, 1e-6)
   return fabs(fm - M) > tol;                         // NaN compares false, as in numpy
@@ -342,7 +350,7 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
       fz = select_f64(sel, p[4 * j + 3], fz);
     }
   }
-  const double fm = frame_mass(fe, fx, fy, fz);
+  const double fm = gen_frame_mass(fe, fx, fy, fz);
   *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
   double q[4 * NS];
   double ws;
