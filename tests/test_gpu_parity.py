@@ -123,6 +123,34 @@ def test_empty_and_ragged_sizes(cuda, hk, oracle):
         assert wm.sum_w == pytest.approx(float(np.sum(ref["weight"])), rel=1e-13)
 
 
+@pytest.mark.parametrize("masses,excess", [((0.13957039, 0.13957039, 0.493677), 1e-12),
+                                           ((0.13957039, 0.13957039, 0.493677), 1e-9),
+                                           ((3.0969, 0.493677), 1e-13),
+                                           ((0.0, 0.0, 0.0), 1.0),
+                                           ((0.0, 0.0), 1.0),
+                                           ((0.0, 0.2, 0.0, 0.1), 0.5)])
+def test_threshold_and_massless_edges_vs_oracle(cuda, hk, oracle, masses, excess):
+    """Edges of the branch-free kernels: breakup lambda tiny or rounded
+    negative just above threshold (np.maximum(lam, 0) as a sign mask, sqrt(+0)
+    through the clamped seed), massless daughters (zero energies and frame
+    masses), and the seed = stream = 0 key whose first uniform is exactly 0
+    (cos theta = -1, sqrt(1 - cz^2) = sqrt(0))."""
+    M = sum(masses) + excess
+    spec, mother = hk.DecaySpec(M, masses), hk.FourVector.at_rest(M)
+    n = 20_000
+    for key in ((0, 0, 0), (5, 3, 0), (0, 0, 12_345)):
+        blk = hk.phsp_generate(spec, mother, n, hk.RngKey(*key))
+        ref = oracle.generate(masses, M, n, *key, threads=4)
+        got = _arr(blk)
+        assert_block_parity(got, np.stack(list(ref.values())), len(masses), f"{masses} +{excess} key {key}")
+        assert np.array_equal(got[0], ref["weight"], equal_nan=True), "weights not bit-exact"
+        # massless + u = 0 gives the reference's 0/0 NaNs (phasespace.py:67-71): same pattern
+        assert np.array_equal(np.isnan(got), np.isnan(np.stack(list(ref.values())))), "NaN pattern"
+    blk = hk.phsp_generate(spec, mother, 1, hk.RngKey(0, 0))
+    assert np.array_equal(np.asarray(blk.column("weight")), oracle.generate(masses, M, 1, 0, 0)["weight"],
+                          equal_nan=True)
+
+
 def test_windows_equal_full_run_rows(cuda, hk):
     """Row offsets (GPU shards) and key.counter windows reproduce rows of a
     one-shot run bit for bit (phasespace.py:106)."""
