@@ -307,3 +307,44 @@ def test_sample_pdf_contracts(cuda, hk):
     assert np.array_equal(a.column("x0"), b.column("x0"))
     with pytest.raises(ValueError):
         hk.sample_pdf(g, hk.BoundedRegion.cube(0, 1, 2), 10, hk.RngKey(1, 0))
+
+
+# --- cli.py:193-204 (cmd_phsp) and cli.py:311-343 (cmd_bench): host callers -
+def test_cli_phsp_sequence_on_the_drop_in(cuda, hk, oracle, tmp_path):
+    """cmd_phsp's body, run against the drop-in: generate with the CLI's
+    phase-space stream, unweight against phsp_max_weight with its unweight
+    stream, write CSV.  The file parses back to the oracle's accepted events:
+    same rows and count, weights 1.0, momenta within 1e-12 * E."""
+    from tests.common import B0_DAUGHTERS, B0_MASS, assert_block_parity
+    stream_phasespace, stream_unweight = 1, 4      # cli.py:50, :53
+    seed, n = 2024, 50_000
+    spec = hk.DecaySpec(B0_MASS, B0_DAUGHTERS)
+    block = hk.phsp_generate(spec, hk.FourVector.at_rest(B0_MASS), n, hk.RngKey(seed, stream=stream_phasespace))
+    w_max = hk.phsp_max_weight(spec)
+    block = hk.phsp_unweight(block, w_max, hk.RngKey(seed, stream=stream_unweight))
+    path = tmp_path / "phsp.csv"
+    path.write_text(block.to_csv())
+    back = hk.read_csv(str(path))
+    ref = oracle.generate(B0_DAUGHTERS, B0_MASS, n, seed, stream_phasespace, threads=4)
+    acc = oracle.unweight_accept(ref["weight"], w_max, seed, stream_unweight)
+    want = np.stack([v[acc] for v in ref.values()])
+    want[0] = 1.0
+    got = np.stack([np.asarray(back.column(c)) for c in back.schema.names])
+    assert back.schema.names == tuple(ref.keys()) and got.shape == want.shape
+    assert np.all(got[0] == 1.0)
+    assert_block_parity(got, want, 3, "cmd_phsp")
+
+
+def test_cli_bench_sequence_on_the_drop_in(cuda, hk):
+    """cmd_bench's body: a toy sample with poisson=False and workers=0, then
+    nll timed at several worker counts -- every worker count returns the same
+    value on the drop-in (workers is accepted and has no effect)."""
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(hk.Parameter("mean", 5.0), hk.Parameter("sigma", 1.0))
+    e = hk.shape_exponential(hk.Parameter("tau", 4.0))
+    model = hk.add_pdfs([hk.Parameter("n_gauss", 5e4), hk.Parameter("n_exp", 5e4)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+    sample = hk.generate_model_sample(model, hk.RngKey(7, stream=2), poisson=False, workers=0)
+    assert len(sample) == 100_000
+    values = {w: hk.nll(model, sample, ["x0"], workers=w) for w in (1, 2, 4, 8)}
+    assert len(set(values.values())) == 1
