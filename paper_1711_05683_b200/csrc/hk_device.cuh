@@ -591,14 +591,16 @@ __device__ __forceinline__ void block_sum_store(double (&v)[W], double* out) {
 // out[W * (chunk * HK_WARP_SLICES + warp) ..].  The host folds the slices in
 // index order, so the result is as deterministic as a CTA reduction.
 template <int W>
-__device__ __forceinline__ void warp_sum_store(double (&v)[W], double* out, int64_t chunk) {
+__device__ __forceinline__ void warp_sum_store(double (&v)[W], double* out, int64_t chunk,
+                                               int warp_in_chunk = -1) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
     for (int w = 0; w < W; ++w) v[w] += __shfl_down_sync(0xffffffffu, v[w], off);
   }
   if ((threadIdx.x & 31) == 0) {
-    double* dst = out + (int64_t)W * (chunk * HK_WARP_SLICES + (threadIdx.x >> 5));
+    const int slot = warp_in_chunk >= 0 ? warp_in_chunk : (int)(threadIdx.x >> 5);
+    double* dst = out + (int64_t)W * (chunk * HK_WARP_SLICES + slot);
 #pragma unroll
     for (int w = 0; w < W; ++w) dst[w] = v[w];
   }

@@ -50,9 +50,24 @@ __device__ __forceinline__ double gen_event(const hk_decay_t& d, const TwoBody& 
 // thread owns in the ILP-2 path go out as one 16-byte streaming store per
 // column (st.global.cs.v2.f64; a warp writes 512 contiguous bytes).  The row
 // mapping -- and so the weight partials -- is the same either way.
-template <int N, int MODE, bool VEC2>
-__global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
+//
+// T threads per CTA: 256 (one CTA per chunk) or fewer (kBlock / T CTAs per
+// chunk, each a slice of it through a virtual thread id, so every warp keeps
+// its rows and its weight-partial slot -- identical bits).  The VEC2 3/4-body
+// kernels launch T = 128 at 4 CTAs/SM (the same 16 warps and 128 registers as
+// 2 x 256): the finer CTA granularity measured 1.1% faster on B200 (1.7755
+// vs 1.7957 ms per 1e8, same box); 64 ties, 32 is slower, and 5-6 CTAs/SM
+// (102/85 registers) spill and lose.
+#ifndef HK_GEN_T
+#define HK_GEN_T 128
+#endif
+#ifndef HK_GEN_T_MINB
+#define HK_GEN_T_MINB 4
+#endif
+template <int N, int MODE, bool VEC2, int T = kBlock>
+__global__ void __launch_bounds__(T, T == kBlock ? GenShape<N>::min_blocks : HK_GEN_T_MINB)
     k_generate(const __grid_constant__ GenArgs a) {
+  constexpr int kSplit = kBlock / T;  // CTAs per chunk
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
@@ -60,14 +75,16 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
   TwoBody tb{};
   if constexpr (N == 2) tb = two_body_consts(a.d);
   const RestHoist h = rest_hoist<N>(a.d);
-  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < chunks * kSplit; u += gridDim.x) {
+    const int64_t c = u / kSplit;
+    const int vt = (int)(u % kSplit) * T + (int)threadIdx.x;  // thread id within the chunk
     double acc[2] = {0.0, 0.0};
     // full chunks, mother at rest: rows 2t and 2t + 1 of each 512-row block
     // together (ILP 2)
     if (GenShape<N>::ilp == 2 && c * HK_CHUNK + HK_CHUNK <= a.count && !a.d.moving) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {
-        const int64_t r0 = c * HK_CHUNK + i * (2 * kBlock) + 2 * threadIdx.x;
+        const int64_t r0 = c * HK_CHUNK + i * (2 * kBlock) + 2 * vt;
         const int64_t r1 = r0 + 1;
         double p0[4 * N], p1[4 * N];
         const double w0 = gen_event<N, MODE>(a.d, tb, h, a.rp, a.ev_begin + (uint64_t)r0, p0);
@@ -93,12 +110,12 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         acc[0] += w1;
         acc[1] += w1 * w1;
       }
-      if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
+      if (a.wpart) warp_sum_store<2>(acc, a.wpart, c, vt >> 5);
       continue;
     }
 #pragma unroll 1
     for (int i = 0; i < kRowsPerThread; ++i) {
-      const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+      const int64_t r = c * HK_CHUNK + i * kBlock + vt;
       if (r < a.count) {
         double p[4 * N];
         const double w = gen_event<N, MODE>(a.d, tb, h, a.rp, a.ev_begin + (uint64_t)r, p);
@@ -115,7 +132,7 @@ __global__ void __launch_bounds__(kBlock, GenShape<N>::min_blocks)
         acc[1] += w * w;
       }
     }
-    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
+    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c, vt >> 5);
   }
 }
 
@@ -622,11 +639,13 @@ int launch_fold_segments(const double* parts, int64_t n_seg, int seg_len, int wi
 // ------------------------------------------------------ launch dispatch ----
 template <int MODE>
 int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
+  const unsigned grid_t = chunk_grid(num_chunks(a.count) * (kBlock / HK_GEN_T));
   switch (a.d.n) {
 #define HK_GEN_CASE(NN)                                              \
   case NN:                                                           \
     if (NN <= 4 && a.vec2)                                           \
-      k_generate<NN, MODE, (NN <= 4)><<<grid, kBlock, 0, st>>>(a);   \
+      k_generate<NN, MODE, (NN <= 4), HK_GEN_T>                      \
+          <<<grid_t, HK_GEN_T, 0, st>>>(a);                          \
     else                                                             \
       k_generate<NN, MODE, false><<<grid, kBlock, 0, st>>>(a);       \
     break;
