@@ -398,8 +398,16 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
 // (Adjacent-row pairing with one double2 store per column, as in k_generate,
 // measured no faster here -- 4.23 vs 4.20 ms per 1.25e8 C3 events: holding
 // both events' 17 outputs for the paired stores spills 64 B at 128 registers.)
+// HK_CHAIN_T threads per CTA, kBlock / HK_CHAIN_T CTAs per chunk through a
+// virtual thread id (rows and weight slots unchanged), as in k_generate:
+// 64 measured 3.576 ms per 1.25e8 C3 events against 3.592 for 256 (same box).
+#ifndef HK_CHAIN_T
+#define HK_CHAIN_T 64
+#endif
 template <int N, int NS, int MODE, int K>
-__global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const __grid_constant__ GenChainArgs a) {
+__global__ void __launch_bounds__(HK_CHAIN_T, HK_CHAIN_MINB * (kBlock / HK_CHAIN_T))
+    k_generate_chain(const __grid_constant__ GenChainArgs a) {
+  constexpr int kSplit = kBlock / HK_CHAIN_T;
   const int64_t chunks = (a.count + HK_CHUNK - 1) / HK_CHUNK;
   Frame mf{};
   if (a.d.moving) mf = make_frame(a.d.mother[0], a.d.mother[1], a.d.mother[2], a.d.mother[3],
@@ -408,12 +416,14 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
   TwoBody tb{};
   if constexpr (NS == 2) tb = two_body_consts(a.sub);
   const RestHoist hp = rest_hoist<N>(a.d);
-  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
+  for (int64_t u = blockIdx.x; u < chunks * kSplit; u += gridDim.x) {
+    const int64_t c = u / kSplit;
+    const int vt = (int)(u % kSplit) * HK_CHAIN_T + (int)threadIdx.x;
     double acc[2] = {0.0, 0.0};
     if (HK_CHAIN_ILP == 2 && N + NS <= 5 && c * HK_CHUNK + HK_CHUNK <= a.count) {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
-        const int64_t r0 = c * HK_CHUNK + i * kBlock + threadIdx.x;
+        const int64_t r0 = c * HK_CHUNK + i * kBlock + vt;
         const double w0 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0, &bad);
         const double w1 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0 + HK_CHUNK / 2, &bad);
         acc[0] += w0;
@@ -424,7 +434,7 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
     } else {
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread; ++i) {
-        const int64_t r = c * HK_CHUNK + i * kBlock + threadIdx.x;
+        const int64_t r = c * HK_CHUNK + i * kBlock + vt;
         if (r < a.count) {
           const double w = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r, &bad);
           acc[0] += w;
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kBlock, HK_CHAIN_MINB) k_generate_chain(const 
         }
       }
     }
-    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c);
+    if (a.wpart) warp_sum_store<2>(acc, a.wpart, c, vt >> 5);
   }
   if (bad != ~0ull) record_bad(a.first_bad, bad);
 }
@@ -711,7 +721,9 @@ int dispatch_chain(const ChainArgs& a, unsigned grid, cudaStream_t st) {
 // chain -- measured no faster on B200: 4.63 vs 4.56 ms per 1.25e8 C3 events.)
 template <int N, int NS, int MODE>
 void launch_gen_chain(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
-  k_generate_chain<N, NS, MODE, -1><<<grid, kBlock, 0, st>>>(a);
+  (void)grid;
+  const unsigned g = chunk_grid(num_chunks(a.count) * (kBlock / HK_CHAIN_T));
+  k_generate_chain<N, NS, MODE, -1><<<g, HK_CHAIN_T, 0, st>>>(a);
 }
 
 template <int MODE, int N>
