@@ -3,10 +3,12 @@
 //
 // Layout in HBM: one contiguous fp64 column per schema field (phsp_schema,
 // phasespace.py:60-64), owned by the caller (torch tensors on the Python side).
-// A CTA owns one 4096-row chunk (parallel.py:18); its 256 threads walk the
-// chunk in 16 row-strided steps so every column store is a fully coalesced
-// 256 B warp transaction, and the chunk's moment partial is a fixed-order
-// CTA reduction -- the GPU analogue of the reference's chunk partials.
+// A 4096-row chunk (parallel.py:18) is walked by 256 threads -- one CTA, or
+// for the generators two / four smaller CTAs through a virtual thread id --
+// in row-strided steps so every column store is a fully coalesced warp
+// transaction, and the chunk's moment partial is a fixed-order reduction
+// (per-warp slots, or a CTA tree) -- the GPU analogue of the reference's
+// chunk partials.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
