@@ -56,6 +56,28 @@ def test_philox_stream_statistics(cuda, hk):
     assert np.mean(u[:1000] != ref) > 0.99
 
 
+def test_philox_uniform_contracts(cuda, hk):
+    """The reference's TestUniform contracts (test_rng.py:10-40), re-run on the
+    Philox stream: deterministic, distinct counters differ, streams separate,
+    key.counter offsets compose with array counters, range and 1e6-draw mean."""
+    key = hk.RngKey(123, stream=0, counter=42)
+    assert hk.uniform(key, rng="philox") == hk.uniform(key, rng="philox")
+    k = hk.RngKey(123)
+    assert hk.uniform(k.at(0), rng="philox") != hk.uniform(k.at(1), rng="philox")
+    idx = np.arange(1000, dtype=np.uint64)
+    a = hk.uniform_array(hk.RngKey(5, stream=0), idx, rng="philox")
+    b = hk.uniform_array(hk.RngKey(5, stream=1), idx, rng="philox")
+    assert np.mean(a != b) > 0.99
+    k = hk.RngKey(9, stream=2)
+    direct = hk.uniform(k.at(1000), rng="philox")
+    shifted = hk.uniform_array(k.at(990), np.array([10], dtype=np.uint64), rng="philox")[0]
+    assert direct == shifted
+    u = hk.uniform_array(hk.RngKey(1), np.arange(100_000, dtype=np.uint64), rng="philox")
+    assert np.all(u >= 0.0) and np.all(u < 1.0)
+    u = hk.uniform_array(hk.RngKey(2024), np.arange(1_000_000, dtype=np.uint64), rng="philox")
+    assert abs(float(np.mean(u)) - 0.5) < 0.002
+
+
 # -------------------------------------------------------------- generation --
 def test_generated_blocks_vs_golden(cuda, hk, golden):
     arrays, scalars = golden
