@@ -246,7 +246,8 @@ def ptr_rows(block) -> ctypes.Array:
     """Column pointers of a 2-D (columns x stride) fp64 block, without
     materialising per-column tensors."""
     base, step = block.data_ptr(), block.stride(0) * block.element_size()
-    return (ctypes.c_void_p * block.shape[0])(*[base + i * step for i in range(block.shape[0])])
+    n = block.shape[0]
+    return (ctypes.c_void_p * n)(*range(base, base + n * step, step))
 
 
 def empty(n: int, dtype=None):
