@@ -98,6 +98,18 @@ def _decay_struct(spec: DecaySpec, mother: tuple, m_mother: float):
     return _lib.make_decay(spec, FourVector(*mother), m_mother)
 
 
+@functools.lru_cache(maxsize=256)
+def _checked_decay(spec: DecaySpec, mother: tuple):
+    """(hk_decay_t, invariant mother mass) per (spec, mother four-vector); the
+    mass check (phasespace.py:175-179) raises, and exceptions are not cached."""
+    m_mother = _check_mother(spec, FourVector(*mother))
+    return _decay_struct(spec, mother, m_mother), m_mother
+
+
+# hk_key_t per (key, mode): RngKey is frozen and the library reads it as const
+_key_struct = functools.lru_cache(maxsize=1024)(_lib.make_key)
+
+
 def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKey,
                   workers: int | None = 1, *, rng: str = "reference",
                   row_offset: int = 0) -> ColumnStore:
@@ -110,12 +122,11 @@ def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKe
     The weight moments (sum w, sum w^2) are fused into the same pass and kept
     in ``store.meta["weight_partials"]``.
     """
-    m_mother = _check_mother(spec, mother)
+    d, _ = _checked_decay(spec, (mother.e, mother.px, mother.py, mother.pz))
     n_events = int(n_events)
     if n_events < 0:
         raise ValueError(f"n_events must be >= 0, got {n_events}")
-    d = _decay_struct(spec, (mother.e, mother.px, mother.py, mother.pz), m_mother)
-    k = _lib.make_key(key, rng_mode(rng))
+    k = _key_struct(key, rng_mode(rng))
     block, wpart = _column_block(4 * spec.n + 1, n_events, 2 * _lib.num_weight_slices(n_events))
     store = ColumnStore._from_block(phsp_schema(spec.n), block, n_events)
     if n_events == 0:
