@@ -270,6 +270,28 @@ def test_fused_chain_equals_two_step(cuda, hk, oracle):
     assert np.array_equal(a, b, equal_nan=True)
 
 
+def test_fused_chain_moving_mother_and_ragged(cuda, hk, oracle):
+    """The fused chain with a boosted parent (the generator's non-ILP boost
+    path) and a ragged size: bit-identical to generate + decay_chain, and
+    within the parity budget of the oracle's generate + decay_chain."""
+    spec = hk.DecaySpec(B0_MASS, B0_DAUGHTERS)
+    p = (0.7, -1.9, 3.3)
+    e = math.sqrt(B0_MASS ** 2 + sum(c * c for c in p))
+    mother = hk.FourVector(e, *p)
+    sub = hk.DecaySpec(M_JPSI, (M_MU, M_MU))
+    n = 3 * 4096 + 1001
+    fused = _arr(hk.phsp_generate_chain(spec, mother, n, hk.RngKey(8, 1), 1, sub, hk.RngKey(9, 1)))
+    two = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, mother, n, hk.RngKey(8, 1)), 1, sub,
+                                   hk.RngKey(9, 1)))
+    assert np.array_equal(fused, two, equal_nan=True)
+    par = oracle.generate(B0_DAUGHTERS, B0_MASS, n, 8, 1, mother=(e, *p), threads=4)
+    ref = oracle.decay_chain(par, 1, (M_MU, M_MU), M_JPSI, 9, 1, threads=4)
+    assert_block_parity(fused, np.stack(list(ref.values())), 4, "moving-mother chain")
+    tot = [sum(fused[1 + 4 * k + c] for k in range(4)) for c in range(4)]
+    for got, want in zip(tot, (e, *p)):
+        assert np.max(np.abs(got - want)) <= 1e-9 * e
+
+
 def test_chain_mass_mismatch_names_event(cuda, hk):
     spec = hk.DecaySpec(2.0, (0.9, 0.3))
     blk = hk.phsp_generate(spec, hk.FourVector.at_rest(2.0), 100, hk.RngKey(20, 1))
