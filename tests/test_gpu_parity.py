@@ -422,6 +422,22 @@ def test_unweight_vs_golden(cuda, hk, golden):
         hk.phsp_unweight(blk, 0.5 * float(np.max(np.asarray(blk.column("weight")))), hk.RngKey(1, 4))
 
 
+@pytest.mark.parametrize("n,offset", [(1, 0), (4095, 0), (4097, 0), (12_289, 7), (50_000, 1_234_567)])
+def test_unweight_ragged_and_offset_vs_oracle(cuda, hk, oracle, n, offset):
+    """Accept masks at ragged sizes and row offsets (the scan/compaction tail
+    and the counter of a shard) equal the oracle's; order is preserved."""
+    spec, mother = _b0(hk)
+    w_max = hk.phsp_max_weight(spec)
+    blk = hk.phsp_generate(spec, mother, n, hk.RngKey(6, 1), row_offset=offset)
+    out = hk.phsp_unweight(blk, w_max, hk.RngKey(6, 4), row_offset=offset)
+    w = np.asarray(blk.column("weight"))
+    acc = oracle.unweight_accept(w, w_max, 6, 4, ev_begin=offset)
+    assert len(out) == int(acc.sum())
+    for c in ("p1_e", "p2_px", "p3_pz"):
+        assert np.array_equal(np.asarray(out.column(c)), np.asarray(blk.column(c))[acc])
+    assert np.all(np.asarray(out.column("weight")) == 1.0)
+
+
 def test_where_mask_on_device(cuda, hk):
     spec, mother = _b0(hk)
     blk = hk.phsp_generate(spec, mother, 20_000, hk.RngKey(2, 1))
