@@ -644,3 +644,29 @@ def test_sharded_runs_bitwise_invariant(cuda, hk):
         assert torch.equal(torch.cat(cols), one.device_column("p2_px"))
         tot = _lib.fold(torch.cat(parts), _lib.num_chunks(n), 2).cpu().numpy()
         assert np.array_equal(tot, ref_tot), world
+
+
+@pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 10_001, 123_457])
+def test_nll_ragged_sizes_and_generic_models_vs_oracle(cuda, hk, oracle, n):
+    """The FCN's tail tile and last-CTA fold at ragged sizes (factored
+    Gaussian + exponential path), and the generic density path (three
+    components: two Gaussians and an exponential) -- both within 1e-10 of the
+    oracle's reference-order NLL."""
+    rs = np.random.default_rng(n)
+    x = np.clip(np.concatenate([rs.normal(5.0, 0.5, n // 2 + 1), rs.exponential(3.0, n)]), 1e-3, 9.999)[:n]
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(hk.Parameter("mean", 5.0), hk.Parameter("sigma", 0.5))
+    e = hk.shape_exponential(hk.Parameter("tau", 3.0))
+    store = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    two = hk.add_pdfs([hk.Parameter("n_sig", 0.4 * n), hk.Parameter("n_bkg", 0.6 * n)],
+                      [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+    want = oracle.nll(x, oracle.gauss_exp_components(5.0, 0.5, 3.0, 0.4 * n, 0.6 * n))
+    assert hk.nll(two, store, ["x0"]) == pytest.approx(want, rel=1e-10, abs=1e-9)
+    g2 = hk.shape_gaussian(hk.Parameter("mean2", 2.0), hk.Parameter("sigma2", 1.5))
+    three = hk.add_pdfs([hk.Parameter("a", 0.3 * n), hk.Parameter("b", 0.2 * n), hk.Parameter("c", 0.5 * n)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(g2, hk.gaussian_norm(g2), region),
+                         hk.make_pdf(e, hk.exponential_norm(e), region)])
+    comps = [("gauss", 0.3 * n, 5.0, 0.5, oracle.gaussian_norm(5.0, 0.5, 0.0, 10.0)),
+             ("gauss", 0.2 * n, 2.0, 1.5, oracle.gaussian_norm(2.0, 1.5, 0.0, 10.0)),
+             ("exp", 0.5 * n, 3.0, oracle.exponential_norm(3.0, 0.0, 10.0))]
+    assert hk.nll(three, store, ["x0"]) == pytest.approx(oracle.nll(x, comps), rel=1e-10, abs=1e-9)
