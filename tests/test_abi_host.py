@@ -344,3 +344,18 @@ class TestStoreAndSharding:
                     assert b0 == a1
                 for a, b in rs:
                     assert a % CHUNK == 0 and a <= b
+
+
+@pytest.mark.parametrize("lang,std", [("c", "-std=c99"), ("c++", "-std=c++17")])
+def test_header_is_plain_c_and_cpp(lang, std):
+    """include/hepkit_cuda.h is the drop-in boundary for C / cgo / JNI hosts:
+    it must compile as pedantic C99 and as C++ with no CUDA or torch types."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc" if lang == "c" else "g++")
+    if cc is None:
+        pytest.skip("no host compiler")
+    hdr = os.path.join(ROOT, "include", "hepkit_cuda.h")
+    r = subprocess.run([cc, std, "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only", "-x", lang, hdr],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
