@@ -351,7 +351,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     C1 1e5 generation through the API; C3 fused chain, 1e9 events sharded
     (1.25e8 per GPU: 1e9/8); C5 fused Dalitz integration of 1e10 events
     split over the GPUs (strong scaling)."""
-    from paper_1711_05683_b200.parallel import gather_partials, shard_range
+    from paper_1711_05683_b200.parallel import sharded_integrate
 
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
     out = {}
@@ -422,21 +422,16 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     del blk
     torch.cuda.empty_cache()
     n5 = 10_000_000_000
-    a, b = shard_range(n5, rank, world)
     res = {}
 
     def c5():
-        parts = hk.phsp_integrate(hk.identity(), spec, mother, b - a, hk.RngKey(1, 1), m12,
-                                  row_offset=a, return_partials=True)
-        full = gather_partials(parts, n5, 5)
-        res["tot"] = _lib.fold(full, _lib.num_chunks(n5), 5)
+        res["r"] = sharded_integrate(hk.identity(), spec, mother, n5, hk.RngKey(1, 1), m12)
 
     dt = _timed(torch, c5, 2, dist)
-    tot = res["tot"].cpu().numpy()
-    mu = tot[1] / tot[0]
     out["C5"] = {"workload": "1e10 B0->J/psi K pi events, fused generation + <m12^2> weighted average, "
-                             f"strong scaling over {world} GPU(s), no event store",
-                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(mu),
+                             f"strong scaling over {world} GPU(s), no event store; 1024 super-chunk records "
+                             "(40 KB) cross GPUs",
+                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(res["r"].value),
                  "roofline": _fp64_roofline("hk_jit_integrate", n5 / dt / world)}
     # C5 secondary integrand: K*(892) Breit-Wigner on m^2_K pi, the named builtin
 
@@ -448,16 +443,12 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         return (e * e - px * px - py * py - pz * pz,)
 
     def c5bw():
-        parts = hk.phsp_integrate(hk.breit_wigner(0.89555, 0.0473), spec, mother, b - a, hk.RngKey(1, 1), m23,
-                                  row_offset=a, return_partials=True)
-        full = gather_partials(parts, n5, 5)
-        res["tot"] = _lib.fold(full, _lib.num_chunks(n5), 5)
+        res["r"] = sharded_integrate(hk.breit_wigner(0.89555, 0.0473), spec, mother, n5, hk.RngKey(1, 1), m23)
 
     dt = _timed(torch, c5bw, 2, dist)
-    tot = res["tot"].cpu().numpy()
     out["C5_bw"] = {"workload": "1e10 events, fused generation + <BW_K*(892)(m^2_K pi)> (M=0.89555, G=0.0473), "
                                 f"strong scaling over {world} GPU(s), no event store",
-                    "value": n5 / dt, "unit": "events/s", "seconds": dt, "bw_average": float(tot[1] / tot[0])}
+                    "value": n5 / dt, "unit": "events/s", "seconds": dt, "bw_average": float(res["r"].value)}
     # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
     # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
     expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
@@ -483,7 +474,7 @@ def run_ours(args) -> None:
 
     import paper_1711_05683_b200 as hk
     from paper_1711_05683_b200 import _lib
-    from paper_1711_05683_b200.parallel import gather_partials
+    from paper_1711_05683_b200.parallel import gather_supers, shard_range, super_span
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -502,8 +493,10 @@ def run_ours(args) -> None:
         else:
             dist.init_process_group(backend)
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
-    n = EVENTS_PER_GPU
-    n_total = n * world
+    n_total = EVENTS_PER_GPU * world
+    row0, row1 = shard_range(n_total, rank, world)    # whole super-chunks: 1e8 rows per rank up to a chunk
+    s0, s1 = super_span(rank, world)
+    n = row1 - row0
     key = hk.RngKey(1, 1)
     d = _lib.make_decay(spec, mother, M_B0)
     k = _lib.make_key(key)
@@ -516,12 +509,12 @@ def run_ours(args) -> None:
     def step(gen_events=None):
         if gen_events:
             gen_events[0].record(st)
-        _lib.check(L.hk_phsp_generate(d, k, rank * n, n, colp, _lib.ptr(wpart), st.cuda_stream), "generate")
+        _lib.check(L.hk_phsp_generate(d, k, row0, n, colp, _lib.ptr(wpart), st.cuda_stream), "generate")
         if gen_events:
             gen_events[1].record(st)
-        local = _lib.weight_chunk_partials(wpart, n)     # per chunk: 8 warp slices -> 1 pair
-        full = gather_partials(local, n_total, 2)          # 16 B per chunk cross GPUs
-        return _lib.fold(full, _lib.num_chunks(n_total), 2)
+        local = _lib.fold_supers(wpart, n_total, s0, s1, _lib.HK_WARP_SLICES, 2)   # warp slices -> supers
+        full, _ = gather_supers(local, 2)                  # 1024 x 16 B cross GPUs
+        return _lib.fold(full, _lib.HK_SUPERS, 2)
 
     for _ in range(args.warmup):
         tot = step()
@@ -594,7 +587,7 @@ def run_ours(args) -> None:
         # the drop-in API as a user calls it: phsp_generate (device-resident
         # store) + phsp_weight_moments (the step's result, 16 B read back)
         def api_step():
-            blk = hk.phsp_generate(spec, mother, n, key, row_offset=rank * n)
+            blk = hk.phsp_generate(spec, mother, n, key, row_offset=row0)
             return hk.phsp_weight_moments(blk)
 
         api_step()
@@ -621,7 +614,7 @@ def run_ours(args) -> None:
             "config": {"workload": "C2: B0->J/psi K pi 3-body phase-space generation + weight integration "
                                    "(sum/mean/variance), 1e8 events per GPU, stored to HBM",
                        "events_per_gpu": n, "events_per_step": n_total, "rng": "reference SplitMix64 stream",
-                       "parallelism": f"dp{world} (contiguous event shards, NCCL gather of chunk partials)",
+                       "parallelism": f"dp{world} (contiguous super-chunk-aligned event shards, NCCL all-gather of 1024 super-chunk records)",
                        "l2": "each step writes 10.4 GB per GPU (> 126 MB L2): no flush needed",
                        "weight_sum": float(sums[0]), "weight_mean": float(sums[0] / n_total),
                        "weight_variance": float(max(sums[1] / n_total - (sums[0] / n_total) ** 2, 0.0))},
@@ -632,7 +625,7 @@ def run_ours(args) -> None:
                          "kernel_ms": gen_avg * 1e3, "kernel_share_of_step": gen_avg / per_step},
             "clocks": clocks.summary(),
             "e2e": e2e,
-            "gpu_launches": 3 * args.steps,   # k_generate + k_fold_segments + k_fold per step
+            "gpu_launches": 3 * args.steps,   # k_generate + k_fold_supers + k_fold per step
             "cpu_baseline": cpu,
             "fcn": fcn,
             "other_configs": others,

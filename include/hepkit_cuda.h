@@ -288,6 +288,23 @@ int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_b
 int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_len, int32_t width,
                      double* d_out, void* stream);
 
+/* Super-chunk fold, the GPU-count-invariant exchange unit (SURVEY.md 8(e)
+ * option ii; replaces the ordered fold of parallel.py:74-92 across devices).
+ * A run's n_chunks_total 4096-row chunks are cut into HK_SUPERS fixed
+ * super-chunks: super s covers global chunks [s*N/S, (s+1)*N/S) (floor).
+ * d_partials holds recs_per_chunk records of `width` doubles per chunk for
+ * global chunks [chunk_begin, chunk_begin + n_chunks_local) -- which must be
+ * exactly supers [s_begin, s_begin + s_count) -- and d_out receives one
+ * record per super (s_count * width doubles), each the fixed-order sum of its
+ * records.  A GPU shard made of whole supers folds them locally; the
+ * HK_SUPERS records (40 KB at width 5) are all-gathered and hk_fold_partials
+ * folds them identically on every device, so totals are bitwise independent
+ * of the device count (1/2/4/8 divide HK_SUPERS). */
+#define HK_SUPERS 1024
+int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chunk_begin,
+                   int64_t n_chunks_local, int32_t recs_per_chunk, int32_t width, int32_t s_begin,
+                   int32_t s_count, double* d_out, void* stream);
+
 /* Deterministic fold of n_parts partials of `width` (<= 32) doubles each
  * (parallel.py:86-92 semantics, fixed tree order) into d_out[width]. */
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,

@@ -43,6 +43,7 @@ EXPORTS = (
     "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
     "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles", "hk_fold_segments",
     "hk_init", "hk_shutdown", "hk_clique_size", "hk_allreduce_partials", "hk_allgather_partials",
+    "hk_fold_supers",
 )
 
 
@@ -134,6 +135,7 @@ _SIGS = {
     "hk_csv_scratch_bytes": (_I64, [_I64, _I32]),
     "hk_nll_work_doubles": (_I64, [_I64]),
     "hk_fold_segments": (_INT, [_P, _I64, _I32, _I32, _P, _P]),
+    "hk_fold_supers": (_INT, [_P, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P]),
     "hk_format_csv": (_INT, [_PP, _I32, _I64, _P, _P, _I64, ctypes.POINTER(_I64), _P]),
     "hk_init": (_INT, [_I32]),
     "hk_shutdown": (_INT, []),
@@ -333,15 +335,46 @@ def fold_segments(partials, n_segments: int, seg_len: int, width: int):
     return out
 
 
+HK_SUPERS = 1024     # super-chunks per run (include/hepkit_cuda.h)
+
+
+def super_chunks(n_total: int, s_begin: int, s_end: int) -> tuple[int, int]:
+    """Global chunk range [c0, c1) of supers [s_begin, s_end) of an n_total-row
+    run: super s covers chunks [s N / S, (s+1) N / S), N = num_chunks(n_total)."""
+    nch = num_chunks(n_total)
+    return s_begin * nch // HK_SUPERS, s_end * nch // HK_SUPERS
+
+
+def fold_supers(partials, n_total: int, s_begin: int, s_end: int, recs_per_chunk: int, width: int):
+    """One record per super-chunk in [s_begin, s_end) from the local per-chunk
+    partials (recs_per_chunk records of `width` doubles per chunk of the
+    supers' chunk range) -> ((s_end - s_begin) * width,) tensor (hk_fold_supers)."""
+    c0, c1 = super_chunks(n_total, s_begin, s_end)
+    out = empty((s_end - s_begin) * width)
+    if s_end > s_begin:
+        p = ptr(partials) if c1 > c0 else None
+        check(lib().hk_fold_supers(p, num_chunks(n_total), c0, c1 - c0, int(recs_per_chunk), int(width),
+                                   int(s_begin), int(s_end - s_begin), ptr(out), stream_ptr()),
+              "hk_fold_supers")
+    return out
+
+
+def total(partials, n: int, width: int, recs_per_chunk: int = 1):
+    """Deterministic total of an n-row run's per-chunk partials: chunks ->
+    HK_SUPERS super-chunks -> one fixed-tree fold.  The same two levels run
+    sharded over any number of GPUs (parallel.py), so totals are bitwise
+    independent of the GPU count."""
+    return fold(fold_supers(partials, n, 0, HK_SUPERS, recs_per_chunk, width), HK_SUPERS, width)
+
+
 def weight_chunk_partials(wpart, n: int):
-    """A generation's per-warp-slice (sum w, sum w^2) -> one pair per 4096-row
-    chunk (the records that cross GPUs); fold them with fold(., num_chunks(n), 2)."""
+    """A generation's per-warp-slice (sum w, sum w^2) -> one pair per 4096-row chunk."""
     return fold_segments(wpart, num_chunks(n), HK_WARP_SLICES, 2)
 
 
 def weight_totals(wpart, n: int):
-    """(sum w, sum w^2) of a generation: slices -> chunks -> total, fixed order."""
-    return fold(weight_chunk_partials(wpart, n), num_chunks(n), 2)
+    """(sum w, sum w^2) of a generation: warp slices -> supers -> total, fixed order."""
+    return total(wpart, n, 2, HK_WARP_SLICES)
 
 
 JIT_OFF, JIT_ALWAYS, JIT_AUTO = 0, 1, 2

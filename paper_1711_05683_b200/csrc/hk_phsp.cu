@@ -648,6 +648,34 @@ int launch_fold_segments(const double* parts, int64_t n_seg, int seg_len, int wi
   return check_launch("k_fold_segments");
 }
 
+// Super-chunk fold (SURVEY.md 8(e) option ii).  The global chunk sequence of
+// a run (nch chunks) is cut into HK_SUPERS fixed super-chunks, super s
+// covering global chunks [s nch / S, (s+1) nch / S) (floor).  GPU shards are
+// whole runs of supers, so every super is folded by exactly one rank from the
+// same records in the same order -- whatever the GPU count -- and only
+// S x width doubles cross GPUs (40 KB for the 5-wide averages).  One warp per
+// super: lane l sums records l, l + 32, ... in order, then a fixed shuffle
+// tree.  The local partial array holds recs records (of `width` doubles) per
+// chunk for global chunks [c0, c0 + nloc), and this launch writes supers
+// [s0, s0 + s_count) (which the caller checks lie inside that range).
+__global__ void __launch_bounds__(256) k_fold_supers(const double* __restrict__ parts, int64_t nch,
+                                                     int64_t c0, int recs, int width, int n_super,
+                                                     int s0, int s_count, double* __restrict__ out) {
+  const int sl = (int)((blockIdx.x * 256ll + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (sl >= s_count) return;
+  const int64_t s = s0 + sl;
+  const int64_t a = (s * nch / n_super - c0) * recs;
+  const int64_t b = ((s + 1) * nch / n_super - c0) * recs;
+  for (int w = 0; w < width; ++w) {
+    double acc = 0.0;
+    for (int64_t j = a + lane; j < b; j += 32) acc += __ldg(parts + j * width + w);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if (lane == 0) out[(int64_t)sl * width + w] = acc;
+  }
+}
+
 // ------------------------------------------------------ launch dispatch ----
 template <int MODE>
 int dispatch_generate(const GenArgs& a, unsigned grid, cudaStream_t st) {
@@ -1034,6 +1062,33 @@ int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_l
   HK_REQUIRE(n_segments >= 0, "negative segment count");
   HK_REQUIRE(n_segments == 0 || (d_partials && d_out), "NULL pointer");
   return launch_fold_segments(d_partials, n_segments, seg_len, width, d_out, as_stream(stream));
+}
+
+int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chunk_begin,
+                   int64_t n_chunks_local, int32_t recs_per_chunk, int32_t width, int32_t s_begin,
+                   int32_t s_count, double* d_out, void* stream) {
+  HK_REQUIRE(width >= 1 && width <= 32 && recs_per_chunk >= 1 && recs_per_chunk <= 1024,
+             "bad record shape %d x %d", recs_per_chunk, width);
+  HK_REQUIRE(n_chunks_total >= 0 && chunk_begin >= 0 && n_chunks_local >= 0 &&
+                 chunk_begin + n_chunks_local <= n_chunks_total,
+             "chunk range [%lld, %lld) outside [0, %lld)", (long long)chunk_begin,
+             (long long)(chunk_begin + n_chunks_local), (long long)n_chunks_total);
+  HK_REQUIRE(s_begin >= 0 && s_count >= 0 && s_begin + s_count <= HK_SUPERS,
+             "super range [%d, %d) outside [0, %d)", s_begin, s_begin + s_count, HK_SUPERS);
+  if (s_count == 0) return HK_OK;
+  // the supers must be exactly the local chunks (a rank folds only its own records)
+  const int64_t first = (int64_t)s_begin * n_chunks_total / HK_SUPERS;
+  const int64_t last = (int64_t)(s_begin + s_count) * n_chunks_total / HK_SUPERS;
+  HK_REQUIRE(first == chunk_begin && last == chunk_begin + n_chunks_local,
+             "supers [%d, %d) cover chunks [%lld, %lld), the partials hold [%lld, %lld)", s_begin,
+             s_begin + s_count, (long long)first, (long long)last, (long long)chunk_begin,
+             (long long)(chunk_begin + n_chunks_local));
+  HK_REQUIRE(d_out && (n_chunks_local == 0 || d_partials), "NULL pointer");
+  const unsigned grid = (unsigned)((s_count * 32 + 255) / 256);
+  k_fold_supers<<<grid, 256, 0, as_stream(stream)>>>(d_partials, n_chunks_total, chunk_begin,
+                                                     recs_per_chunk, width, HK_SUPERS, s_begin,
+                                                     s_count, d_out);
+  return check_launch("k_fold_supers");
 }
 
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,

@@ -112,9 +112,9 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
   const int ncols = 4 * spec->n + 1;
   const int64_t chunks = num_chunks(ev_count);
-  // stage layout: [partials: 2 doubles per warp-slice][chunk partials: 2 per chunk]
+  // stage layout: [partials: 2 doubles per warp-slice][super records: 2 per super]
   //               [sum cell: 2 doubles][2 x piece buffers]
-  const size_t head = (size_t)(chunks * 2 * HK_WARP_SLICES + chunks * 2 + 2) * sizeof(double);
+  const size_t head = (size_t)(chunks * 2 * HK_WARP_SLICES + HK_SUPERS * 2 + 2) * sizeof(double);
   HK_REQUIRE(stage_bytes > head, "staging area too small");
   const size_t per_row = (size_t)ncols * sizeof(double);
   int64_t piece = (int64_t)((stage_bytes - head) / (2 * per_row));
@@ -129,7 +129,7 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
   cudaStream_t st = as_stream(stream);
   double* part = static_cast<double*>(d_stage);
   double* cpart = part + chunks * 2 * HK_WARP_SLICES;
-  double* sums = cpart + chunks * 2;
+  double* sums = cpart + HK_SUPERS * 2;
   double* buf[2] = {sums + 2, sums + 2 + piece * ncols};
   for (int64_t off = 0, i = 0; off < ev_count; off += piece, ++i) {
     const int b = (int)(i & 1);
@@ -147,9 +147,10 @@ int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t 
                               cudaMemcpyDeviceToHost, L->copy));
     HK_CUDA(cudaEventRecord(L->freed[b], L->copy));
   }
-  // the same two-level fold as phsp_weight_moments: slices -> chunks -> total
-  if (int rc = launch_fold_segments(part, chunks, HK_WARP_SLICES, 2, cpart, st)) return rc;
-  if (int rc = launch_fold(cpart, chunks, 2, sums, st)) return rc;
+  // the same two-level fold as phsp_weight_moments: slices -> supers -> total
+  if (int rc = hk_fold_supers(part, chunks, 0, chunks, HK_WARP_SLICES, 2, 0, HK_SUPERS, cpart, stream))
+    return rc;
+  if (int rc = launch_fold(cpart, HK_SUPERS, 2, sums, st)) return rc;
   HK_CUDA(cudaStreamSynchronize(L->copy));
   if (h_wsums) {
     HK_CUDA(cudaMemcpyAsync(h_wsums, sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -3,27 +3,39 @@
 The reference splits every bulk operation into fixed 65 536-row batches and
 4096-row chunk partials folded in a fixed order, so results do not depend on
 the worker count.  Here the "workers" are GPUs, one process per GPU
-(torch.distributed, NCCL over NVLink/NVSwitch):
+(torch.distributed, NCCL over NVLink/NVSwitch), and the exchange follows
+SURVEY.md 8(e) option (ii):
 
-* events shard as contiguous, chunk-aligned global row ranges
-  (``shard_range``); each rank generates/evaluates its range with the
-  *global* row index, so shards are bit-identical to the same rows of a
-  one-GPU run (RNG counters are global, phasespace.py:105-109);
-* the only exchange is the chunk partials: ``gather_partials`` all-gathers
-  them (a few KB per rank) into global chunk order and every rank folds the
-  same array with the same fixed tree -- so the reduced value is bitwise
-  independent of the number of GPUs (the analogue of the reference's
-  worker-invariance tests, test_phasespace.py:87-93, test_fitting.py:120-124).
+* a run's chunks are cut into HK_SUPERS = 1024 fixed super-chunks
+  (``_lib.super_chunks``); rank r of W owns supers [1024 r / W, 1024 (r+1) / W)
+  and so a contiguous, chunk-aligned row range (``shard_range``).  Each rank
+  generates/evaluates its range with the *global* row index, so shards are
+  bit-identical to the same rows of a one-GPU run (RNG counters are global,
+  phasespace.py:105-109);
+* each rank folds its chunk partials into one record per super-chunk on the
+  device (hk_fold_supers), and the only exchange is those records:
+  ``gather_supers`` all-gathers 1024 x width doubles (40 KB for the 5-wide
+  averages, whatever the event count), and every rank folds the same array
+  with the same fixed tree.  A one-GPU total (``_lib.total``) runs the same
+  two levels, so every reduced value is bitwise independent of the GPU count
+  (the analogue of the reference's worker-invariance tests,
+  test_phasespace.py:87-93, test_fitting.py:120-124);
+* per-rank error rows travel with the records, so a bad event on one rank
+  raises the same exception on every rank instead of leaving the others
+  waiting in the collective.
 """
 
 from __future__ import annotations
 
 import os
 
+import numpy as np
+
 from . import _lib
 
 CHUNK = _lib.HK_CHUNK          # parallel.py:18
 EVAL_BATCH = 16 * CHUNK        # parallel.py:21
+SUPERS = _lib.HK_SUPERS
 
 
 def resolve_workers(workers: int | None) -> int:
@@ -45,13 +57,21 @@ def chunk_bounds(start: int, stop: int, chunk: int = CHUNK) -> list[tuple[int, i
             if max(s, start) < min(s + chunk, stop)]
 
 
-def shard_range(n: int, rank: int, world: int, chunk: int = CHUNK) -> tuple[int, int]:
-    """Contiguous chunk-aligned [a, b) of rank's rows; shards cover [0, n)."""
+def super_span(rank: int, world: int) -> tuple[int, int]:
+    """Super-chunks [s0, s1) owned by `rank` of `world`."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"bad rank {rank} of {world}")
-    nch = (n + chunk - 1) // chunk
-    c0 = nch * rank // world
-    c1 = nch * (rank + 1) // world
+    return SUPERS * rank // world, SUPERS * (rank + 1) // world
+
+
+def shard_range(n: int, rank: int, world: int, chunk: int = CHUNK) -> tuple[int, int]:
+    """Contiguous chunk-aligned [a, b) of rank's rows: the rows of its
+    super-chunks.  Shards cover [0, n); for world | 1024 this is the even
+    chunk split [N r / W, N (r+1) / W) chunks."""
+    if chunk != CHUNK:
+        raise ValueError(f"shards are cut on {CHUNK}-row chunks")
+    s0, s1 = super_span(rank, world)
+    c0, c1 = _lib.super_chunks(n, s0, s1)
     return min(c0 * chunk, n), min(c1 * chunk, n)
 
 
@@ -64,56 +84,97 @@ def dist_info(group=None) -> tuple[int, int]:
     return 0, 1
 
 
-def gather_partials(local, n_total: int, width: int, group=None):
-    """All-gather per-chunk partials (local: flat tensor of this rank's chunks
-    x width) into global chunk order on every rank.
+def _all_gather_padded(local, sizes: list[int], group=None) -> list:
+    """All-gather 1-D tensors of the given per-rank sizes; returns the ranks'
+    tensors (on local's device) in rank order.  NCCL gathers device tensors in
+    place; CPU backends (gloo) go through host memory."""
+    torch = _lib.torch()
+    dist = torch.distributed
+    rank, world = dist_info(group)
+    if local.numel() != sizes[rank]:
+        raise ValueError(f"rank {rank} holds {local.numel()} values, the layout expects {sizes[rank]}")
+    dev = local.device if dist.get_backend(group) == "nccl" else "cpu"
+    cap = max(sizes)
+    if all(sz == cap for sz in sizes):
+        buf = local.to(dev).contiguous()
+    else:
+        buf = torch.zeros(cap, dtype=local.dtype, device=dev)
+        buf[: local.numel()] = local.to(dev)
+    out = torch.empty(world * cap, dtype=local.dtype, device=dev)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    return [out[r * cap: r * cap + sizes[r]].to(local.device) for r in range(world)]
 
-    Shards are chunk-aligned, so the concatenation of the ranks' partials in
-    rank order is exactly the global chunk sequence.  Unequal shard sizes are
-    padded to the largest and trimmed after the gather.
-    """
+
+def gather_supers(local, width: int, group=None, extra=None):
+    """All-gather this rank's super-chunk records (flat, (s1 - s0) x width)
+    into global super order on every rank: (1024 x width tensor, and with
+    `extra` -- a small per-rank float64 vector such as error rows -- the
+    ranks' extras as a (world, len) numpy array)."""
     torch = _lib.torch()
     rank, world = dist_info(group)
+    k = 0 if extra is None else len(extra)
     if world == 1:
-        return local
-    dist = torch.distributed
-    nch = (n_total + CHUNK - 1) // CHUNK
-    sizes = [(nch * (r + 1) // world - nch * r // world) for r in range(world)]
-    cap = max(sizes) * width
-    # NCCL gathers device tensors in place; CPU backends (gloo) go through host memory
-    dev = local.device if dist.get_backend(group) == "nccl" else "cpu"
-    buf = torch.zeros(cap, dtype=local.dtype, device=dev)
-    buf[: local.numel()] = local.to(dev)
-    out = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(out, buf, group=group)
-    return torch.cat([o[: s * width] for o, s in zip(out, sizes)]).to(local.device)
+        ex = None if extra is None else np.asarray(extra, dtype=np.float64).reshape(1, k)
+        return local, ex
+    sizes = [(b - a) * width + k for a, b in (super_span(r, world) for r in range(world))]
+    mine = local
+    if k:
+        mine = torch.cat([local, torch.tensor(list(extra), dtype=torch.float64, device=local.device)])
+    parts = _all_gather_padded(mine, sizes, group)
+    full = torch.cat([p[: p.numel() - k] for p in parts])
+    ex = None
+    if k:
+        ex = torch.stack([p[p.numel() - k:] for p in parts]).cpu().numpy()
+    return full, ex
+
+
+def _min_row(rows) -> int:
+    """Smallest valid global row among float-encoded rows (-1 = none)."""
+    valid = [int(r) for r in rows if r >= 0]
+    return min(valid) if valid else _lib.HK_NO_BAD_ROW
 
 
 def sharded_weight_moments(block_shard, n_total: int, group=None):
-    """Global (sum w, sum w^2) of a sharded generation: gather + same fold."""
-    parts = block_shard.meta["weight_partials"]   # 2 doubles per warp-slice, 8 slices per chunk
-    # fold each chunk's 8 slices locally (fixed order), so only one record per
-    # chunk crosses GPUs; every rank then folds the same global chunk sequence
-    local = _lib.weight_chunk_partials(parts, len(block_shard))
-    full = gather_partials(local, n_total, 2, group)
-    return _lib.fold(full, _lib.num_chunks(n_total), 2)
+    """Global (sum w, sum w^2) of a sharded generation (device tensor of 2):
+    the shard's warp-slice partials -> its super-chunk records -> gather ->
+    the same fixed fold on every rank.  An empty shard contributes zero
+    records.  Equal bit for bit to phsp_weight_moments of the one-GPU run."""
+    from .phasespace import _weight_partials  # noqa: PLC0415
+    rank, world = dist_info(group)
+    a, b = shard_range(n_total, rank, world)
+    if len(block_shard) != b - a:
+        raise ValueError(f"rank {rank} shard holds {len(block_shard)} rows, shard_range gives {b - a}")
+    parts = _weight_partials(block_shard)
+    if parts is None and b > a:
+        raise ValueError("the shard carries no fused weight partials (generate it with phsp_generate)")
+    s0, s1 = super_span(rank, world)
+    local = _lib.fold_supers(parts, n_total, s0, s1, _lib.HK_WARP_SLICES, 2)
+    full, _ = gather_supers(local, 2, group)
+    return _lib.fold(full, SUPERS, 2)
 
 
 def sharded_integrate(expr, spec, mother, n_total: int, key, arg_builder, group=None,
                       rng: str = "reference"):
     """phsp_integrate over n_total events sharded across the process group
-    (config C5 at 1/2/4/8 GPUs); returns the IntegrationResult on every rank."""
-    from .phasespace import _finish_average, phsp_integrate  # noqa: PLC0415
+    (config C5 at 1/2/4/8 GPUs); returns the IntegrationResult on every rank,
+    bitwise the same for any GPU count.  The first bad rows of every rank
+    ride along with the super records, so all ranks raise the reference's
+    exception for the globally first bad event together."""
+    from .phasespace import _finish_average, _IntegrateRun  # noqa: PLC0415
 
+    n_total = int(n_total)
+    if n_total == 0:
+        raise ValueError("cannot average over an empty block")
     rank, world = dist_info(group)
     a, b = shard_range(n_total, rank, world)
-    if b > a:
-        parts = phsp_integrate(expr, spec, mother, b - a, key, arg_builder, rng=rng,
-                               row_offset=a, return_partials=True)
-    else:
-        parts = _lib.empty(0)
-    full = gather_partials(parts, n_total, 5, group)
-    tot = _lib.fold(full, (n_total + CHUNK - 1) // CHUNK, 5)
+    run = _IntegrateRun(expr, spec, mother, key, arg_builder, rng)
+    parts, flags = run.partials(b - a, a)
+    s0, s1 = super_span(rank, world)
+    local = _lib.fold_supers(parts, n_total, s0, s1, 1, 5)
+    rows = [-1.0 if f == _lib.HK_NO_BAD_ROW else float(f) for f in flags]
+    full, ex = gather_supers(local, 5, group, extra=rows)
+    run.raise_error([_min_row(ex[:, 0]), _min_row(ex[:, 1])])
+    tot = _lib.fold(full, SUPERS, 5)
     return _finish_average(tot.cpu().numpy(), n_total)
 
 

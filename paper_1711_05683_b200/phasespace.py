@@ -129,12 +129,26 @@ def phsp_generate(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKe
     k = _key_struct(key, rng_mode(rng))
     block, wpart = _column_block(4 * spec.n + 1, n_events, 2 * _lib.num_weight_slices(n_events))
     store = ColumnStore._from_block(phsp_schema(spec.n), block, n_events)
-    if n_events == 0:
-        return store
-    _lib.check(_lib.lib().hk_phsp_generate(d, k, _lib.u64(row_offset), n_events, _lib.ptr_rows(block),
-                                           _lib.ptr(wpart), _lib.stream_ptr()), "hk_phsp_generate")
-    store.meta["weight_partials"] = wpart
+    if n_events:
+        _lib.check(_lib.lib().hk_phsp_generate(d, k, _lib.u64(row_offset), n_events, _lib.ptr_rows(block),
+                                               _lib.ptr(wpart), _lib.stream_ptr()), "hk_phsp_generate")
+    _set_weight_partials(store, wpart)
     return store
+
+
+def _set_weight_partials(store: ColumnStore, wpart) -> None:
+    """Keep a generation's fused (sum w, sum w^2) warp-slice partials with the
+    row count they describe (an empty shard keeps an empty tensor)."""
+    store.meta["weight_partials"] = wpart
+    store.meta["weight_partials_rows"] = len(store)
+
+
+def _weight_partials(store: ColumnStore):
+    """The fused weight partials when they still describe the store's rows."""
+    parts = store.meta.get("weight_partials")
+    if parts is None or store.meta.get("weight_partials_rows") != len(store):
+        return None
+    return parts
 
 
 def phsp_generate_to_host(spec: DecaySpec, mother: FourVector, n_events: int, key: RngKey,
@@ -153,7 +167,7 @@ def phsp_generate_to_host(spec: DecaySpec, mother: FourVector, n_events: int, ke
     ncols = 4 * spec.n + 1
     if out is None:
         out = [torch.empty(n_events, dtype=torch.float64, pin_memory=True) for _ in range(ncols)]
-    head = (2 * _lib.num_weight_slices(n_events) + 2 * _lib.num_chunks(n_events) + 2) * 8
+    head = (2 * _lib.num_weight_slices(n_events) + 2 * _lib.HK_SUPERS + 2) * 8
     stage_bytes = max(int(stage_bytes), head + 2 * ncols * 8 * _lib.HK_CHUNK)
     sums = (ctypes.c_double * 2)()
     with _stage_lock:                     # one staging buffer per device, one user at a time
@@ -217,11 +231,11 @@ def phsp_weight_moments(block: ColumnStore) -> WeightMoments:
     n = len(block)
     if n == 0:
         raise ValueError("cannot integrate an empty block")
-    parts = block.meta.get("weight_partials")
+    parts = _weight_partials(block)
     if parts is None:
         prog = _weight_program()
         parts5 = _moment_partials(block, prog)
-        tot = _lib.fold(parts5, _lib.num_chunks(n), 5).cpu().numpy()
+        tot = _lib.total(parts5, n, 5).cpu().numpy()
         return WeightMoments(n, float(tot[0]), float(tot[2]))
     tot = _lib.weight_totals(parts, n).cpu().numpy()
     return WeightMoments(n, float(tot[0]), float(tot[1]))
@@ -235,9 +249,22 @@ def _weight_program():
 # ---------------------------------------------------------------------------
 # averages
 
+def _weighted_names(block: ColumnStore) -> list[str]:
+    """Column names as the moment kernels see them: they read the weight from
+    column 0 (phsp_schema order, phasespace.py:60-64).  The reference reads it
+    by name (block.column("weight"), phasespace.py:310), so a store whose
+    weight is elsewhere gets a copy of its pointer in front and the traced
+    program's column indices shift by one."""
+    names = list(block.schema.names)
+    if "weight" not in names:
+        raise KeyError("unknown column 'weight'")
+    return names if names[0] == "weight" else ["\0weight", *names]
+
+
 def _moment_partials(block: ColumnStore, prog, bad=None):
     n = len(block)
-    cols = block.device_columns()
+    names = _weighted_names(block)
+    cols = block.device_columns([nm if nm != "\0weight" else "weight" for nm in names])
     parts = _lib.empty(5 * _lib.num_chunks(n))
     _lib.check(_lib.lib().hk_phsp_moments(_lib.ptr_array(cols), len(cols), n, prog, _lib.ptr(parts),
                                           _lib.ptr(bad) if bad is not None else None,
@@ -280,15 +307,15 @@ def phsp_average(expr: FunctorExpr, block: ColumnStore, arg_builder,
     n = len(block)
     if n == 0:
         raise ValueError("cannot average over an empty block")
-    names = block.schema.names
+    names = _weighted_names(block)
     prog, args = lower_average(expr, arg_builder, names)
     bad = _lib.bad_cells(2)
     parts = _moment_partials(block, prog, bad)
-    tot = _lib.fold(parts, _lib.num_chunks(n), 5)
+    tot = _lib.total(parts, n, 5)
     flags = _lib.read_bad(bad)
 
     def row_values(r):
-        return {c: float(block.device_column(names[c])[r]) for c in columns_used(args)}
+        return {c: float(block.device_column(names[c].lstrip("\0"))[r]) for c in columns_used(args)}
 
     _raise_program_error(flags, args, row_values)
     return _finish_average(tot.cpu().numpy(), n)
@@ -303,34 +330,54 @@ def phsp_integrate(expr: FunctorExpr, spec: DecaySpec, mother: FourVector, n_eve
     ``phsp_average(expr, phsp_generate(spec, mother, n_events, key), arg_builder)``
     but reads and writes no event memory.  With ``return_partials`` the
     per-chunk moment partials (device tensor, 5 per 4096 rows) are returned
-    instead, for a multi-GPU fold.
+    instead.
     """
-    m_mother = _check_mother(spec, mother)
     n_events = int(n_events)
     if n_events == 0:
         raise ValueError("cannot average over an empty block")
-    names = phsp_schema(spec.n).names
-    prog, args, root = lower_average(expr, arg_builder, names, with_root=True)
-    pair = match_pair_integrand(root, spec.n)     # Dalitz m^2_ij / BW(m^2_ij): specialised path
-    d = _lib.make_decay(spec, mother, m_mother)
-    k = _lib.make_key(key, rng_mode(rng))
-    bad = _lib.bad_cells(2)
-    parts = _lib.empty(5 * _lib.num_chunks(n_events))
-    _lib.check(_lib.lib().hk_phsp_integrate(d, k, _lib.u64(row_offset), n_events, prog, pair,
-                                            _lib.ptr(parts), _lib.ptr(bad), _lib.stream_ptr()),
-               "hk_phsp_integrate")
-    flags = _lib.read_bad(bad)
-
-    def row_values(r):
-        one = phsp_generate(spec, mother, 1, key, rng=rng, row_offset=r)
-        return {c: float(one.device_column(names[c])[0]) for c in columns_used(args)}
-
-    _raise_program_error([f - row_offset if f != _lib.HK_NO_BAD_ROW else f for f in flags],
-                         args, lambda r: row_values(r + row_offset))
+    run = _IntegrateRun(expr, spec, mother, key, arg_builder, rng)
+    parts, flags = run.partials(n_events, row_offset)
+    run.raise_error(flags, row_offset)
     if return_partials:
         return parts
-    tot = _lib.fold(parts, _lib.num_chunks(n_events), 5)
+    tot = _lib.total(parts, n_events, 5)
     return _finish_average(tot.cpu().numpy(), n_events)
+
+
+class _IntegrateRun:
+    """One fused generate -> f -> moments run, split so that a sharded caller
+    (parallel.sharded_integrate) can exchange partials and error rows before
+    any rank raises."""
+
+    def __init__(self, expr, spec, mother, key, arg_builder, rng):
+        self.m_mother = _check_mother(spec, mother)
+        self.spec, self.mother, self.key, self.rng = spec, mother, key, rng
+        self.names = phsp_schema(spec.n).names
+        self.prog, self.args, root = lower_average(expr, arg_builder, self.names, with_root=True)
+        self.pair = match_pair_integrand(root, spec.n)   # Dalitz m^2_ij / BW(m^2_ij): specialised path
+
+    def partials(self, n_events: int, row_offset: int):
+        """(per-chunk partials, [first zero-divisor row, first non-finite row])
+        of rows [row_offset, row_offset + n_events), rows global."""
+        d = _lib.make_decay(self.spec, self.mother, self.m_mother)
+        k = _lib.make_key(self.key, rng_mode(self.rng))
+        bad = _lib.bad_cells(2)
+        parts = _lib.empty(5 * _lib.num_chunks(n_events))
+        if n_events:
+            _lib.check(_lib.lib().hk_phsp_integrate(d, k, _lib.u64(row_offset), n_events, self.prog,
+                                                    self.pair, _lib.ptr(parts), _lib.ptr(bad),
+                                                    _lib.stream_ptr()), "hk_phsp_integrate")
+        return parts, _lib.read_bad(bad)
+
+    def raise_error(self, flags, base: int = 0) -> None:
+        """The reference's exception for the first bad rows, if any; events
+        are numbered from row `base` (the first row of the averaged block)."""
+        def row_values(r):
+            one = phsp_generate(self.spec, self.mother, 1, self.key, rng=self.rng, row_offset=r + base)
+            return {c: float(one.device_column(self.names[c])[0]) for c in columns_used(self.args)}
+
+        rel = [f if f == _lib.HK_NO_BAD_ROW else f - _lib.u64(base) for f in flags]
+        _raise_program_error(rel, self.args, row_values)
 
 
 # ---------------------------------------------------------------------------
@@ -406,7 +453,7 @@ def phsp_generate_chain(spec: DecaySpec, mother: FourVector, n_events: int, key:
         parent = phsp_generate(spec, mother, 1, key, rng=rng, row_offset=first)
         p4 = [float(parent.device_column(f"p{daughter_index}_{c}")[0]) for c in ("e", "px", "py", "pz")]
         raise _chain_mass_error(daughter_index, *p4, subspec.mother_mass, j)
-    store.meta["weight_partials"] = wpart
+    _set_weight_partials(store, wpart)
     return store
 
 

@@ -48,7 +48,7 @@ def test_allreduce_and_allgather_one_device(clique):
 
 
 def test_gathered_chunk_partials_fold_like_one_device(hk, clique):
-    """Generation weight partials -> per-chunk records -> allgather -> fold,
+    """Generation weight partials -> super-chunk records -> allgather -> fold,
     bit-identical to weight_totals of the same block."""
     import torch
     n = 64 * 4096
@@ -60,17 +60,20 @@ def test_gathered_chunk_partials_fold_like_one_device(hk, clique):
     clique.check(clique.lib().hk_phsp_generate(d, k, 0, n, clique.ptr_array(cols), clique.ptr(wpart),
                                                clique.stream_ptr()), "generate")
     total = clique.weight_totals(wpart, n)
-    chunks = clique.weight_chunk_partials(wpart, n)
-    (gathered,) = clique.allgather_partials([chunks])
-    folded = clique.fold(gathered, clique.num_chunks(n), 2)
+    supers = clique.fold_supers(wpart, n, 0, clique.HK_SUPERS, clique.HK_WARP_SLICES, 2)
+    (gathered,) = clique.allgather_partials([supers])
+    folded = clique.fold(gathered, clique.HK_SUPERS, 2)
     torch.cuda.synchronize()
     assert torch.equal(folded, total)
     w = cols[0].double()
     assert folded[0].item() == pytest.approx(w.sum().item(), rel=1e-12)
     assert folded[1].item() == pytest.approx((w * w).sum().item(), rel=1e-12)
-    # two "devices" holding 32 chunks each: concatenation in device order is the same sequence
-    halves = [chunks[: chunks.numel() // 2], chunks[chunks.numel() // 2:]]
-    assert torch.equal(clique.fold(torch.cat(halves), clique.num_chunks(n), 2), total)
+    # two "devices" holding 32 chunks (512 supers) each: their super records in device order
+    # are the same sequence
+    half = clique.num_weight_slices(n)  # 2 doubles per slice: the first half of wpart is chunks 0..31
+    halves = [clique.fold_supers(wpart[:half], n, 0, 512, clique.HK_WARP_SLICES, 2),
+              clique.fold_supers(wpart[half:], n, 512, 1024, clique.HK_WARP_SLICES, 2)]
+    assert torch.equal(clique.fold(torch.cat(halves), clique.HK_SUPERS, 2), total)
 
 
 def test_shutdown_releases_and_library_stays_usable(hk, cuda):

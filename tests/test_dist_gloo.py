@@ -1,6 +1,6 @@
 """Multi-process (world size 2, gloo, CPU) coverage of the N>1 host logic:
-chunk-aligned shards and the all-gather of per-chunk partials into global
-chunk order (paper_1711_05683_b200/parallel.py).  The GPU box has one GPU,
+super-chunk-aligned shards and the all-gather of super-chunk records into
+global order (paper_1711_05683_b200/parallel.py).  The GPU box has one GPU,
 so the NCCL path is exercised with the same code under gloo here."""
 
 from __future__ import annotations
@@ -21,41 +21,45 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _partials_for(a: int, b: int, width: int) -> np.ndarray:
-    """Deterministic fake partials: value encodes (global chunk, slot)."""
-    from paper_1711_05683_b200.parallel import CHUNK
-    chunks = range(a // CHUNK, (b + CHUNK - 1) // CHUNK)
-    return np.array([[c * 10.0 + w for w in range(width)] for c in chunks], dtype=np.float64).ravel()
+def _supers_for(s0: int, s1: int, width: int) -> np.ndarray:
+    """Deterministic fake super-chunk records: value encodes (super, slot)."""
+    return np.array([[s * 10.0 + w for w in range(width)] for s in range(s0, s1)], dtype=np.float64).ravel()
 
 
 def _worker(rank: int, world: int, port: int, n_total: int, width: int, out_dir: str) -> None:
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1711_05683_b200.parallel import dist_info, gather_partials, shard_range
+        from paper_1711_05683_b200.parallel import dist_info, gather_supers, shard_range, super_span
         r, w = dist_info()
         assert (r, w) == (rank, world)
+        s0, s1 = super_span(rank, world)
+        local = torch.from_numpy(_supers_for(s0, s1, width))
         a, b = shard_range(n_total, rank, world)
-        local = torch.from_numpy(_partials_for(a, b, width))
-        full = gather_partials(local, n_total, width).numpy()
-        np.save(os.path.join(out_dir, f"rank{rank}.npy"), full)
+        full, ex = gather_supers(local, width, extra=[float(a), float(b), -1.0])
+        np.save(os.path.join(out_dir, f"rank{rank}.npy"), full.numpy())
+        np.save(os.path.join(out_dir, f"extra{rank}.npy"), ex)
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("n_total", [1, 4096 * 5, 4096 * 7 + 3, 1_000_003])
-def test_gather_partials_global_order(tmp_path, n_total):
-    from paper_1711_05683_b200.parallel import CHUNK
-    world, width = 2, 5
+def test_gather_supers_global_order(tmp_path, world, n_total):
+    """Every rank receives the 1024 super-chunk records in global order (and
+    the per-rank extras in rank order), including uneven super spans (world 3)
+    and ranks whose row shard is empty (n_total smaller than world chunks)."""
+    from paper_1711_05683_b200.parallel import SUPERS, shard_range
+    width = 5
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, n_total, width, str(tmp_path)), nprocs=world,
                        join=True, start_method="spawn")
-    want = _partials_for(0, n_total, width)
-    nch = (n_total + CHUNK - 1) // CHUNK
-    assert want.size == nch * width
+    want = _supers_for(0, SUPERS, width)
+    shards = np.array([[*shard_range(n_total, r, world), -1.0] for r in range(world)])
     for rank in range(world):
         got = np.load(tmp_path / f"rank{rank}.npy")
         assert np.array_equal(got, want), rank
+        assert np.array_equal(np.load(tmp_path / f"extra{rank}.npy"), shards), rank
 
 
 class _Shard:

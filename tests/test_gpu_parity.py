@@ -626,24 +626,58 @@ def test_sample_pdf_gaussian_ks(cuda, hk):
 # ------------------------------------------------- GPU-count invariance ----
 def test_sharded_runs_bitwise_invariant(cuda, hk):
     """Shards generated separately (what N GPUs do) concatenate to the
-    one-shot block, and the gathered chunk partials fold to the same bits."""
+    one-shot block, and their super-chunk records (hk_fold_supers, 1024 per
+    run) fold to the same bits as the one-GPU total -- for weight moments and
+    for a fused C5-style integration, at 2, 3, 4 and 8 shards."""
     from paper_1711_05683_b200 import _lib
-    from paper_1711_05683_b200.parallel import shard_range
+    from paper_1711_05683_b200.parallel import shard_range, super_span
+    from paper_1711_05683_b200.phasespace import _IntegrateRun
     torch = cuda
     spec, mother = _b0(hk)
     n = 2_000_003
     one = hk.phsp_generate(spec, mother, n, hk.RngKey(1, 1))
     ref_tot = _lib.weight_totals(one.meta["weight_partials"], n).cpu().numpy()
-    for world in (2, 4, 8):
-        parts, cols = [], []
+    ref_avg = hk.phsp_integrate(hk.identity(), spec, mother, n, hk.RngKey(1, 1), m12sq_builder)
+    run = _IntegrateRun(hk.identity(), spec, mother, hk.RngKey(1, 1), m12sq_builder, "reference")
+    for world in (2, 3, 4, 8):
+        wsup, asup, cols = [], [], []
         for r in range(world):
             a, b = shard_range(n, r, world)
+            s0, s1 = super_span(r, world)
             s = hk.phsp_generate(spec, mother, b - a, hk.RngKey(1, 1), row_offset=a)
-            parts.append(_lib.weight_chunk_partials(s.meta["weight_partials"], b - a))
+            wsup.append(_lib.fold_supers(s.meta["weight_partials"], n, s0, s1, _lib.HK_WARP_SLICES, 2))
             cols.append(s.device_column("p2_px"))
+            parts, flags = run.partials(b - a, a)
+            assert flags == [_lib.HK_NO_BAD_ROW] * 2
+            asup.append(_lib.fold_supers(parts, n, s0, s1, 1, 5))
         assert torch.equal(torch.cat(cols), one.device_column("p2_px"))
-        tot = _lib.fold(torch.cat(parts), _lib.num_chunks(n), 2).cpu().numpy()
+        tot = _lib.fold(torch.cat(wsup), _lib.HK_SUPERS, 2).cpu().numpy()
         assert np.array_equal(tot, ref_tot), world
+        avg = _lib.fold(torch.cat(asup), _lib.HK_SUPERS, 5).cpu().numpy()
+        assert avg[1] / avg[0] == ref_avg.value, world
+
+
+def test_sharded_api_single_rank_matches_api(cuda, hk):
+    """parallel.sharded_weight_moments / sharded_integrate without a process
+    group (world 1) return the one-GPU API's bits, including an empty run's
+    error and a store whose partials went stale after push()."""
+    from paper_1711_05683_b200 import parallel
+    spec, mother = _b0(hk)
+    n = 300_017
+    blk = hk.phsp_generate(spec, mother, n, hk.RngKey(1, 1))
+    wm = hk.phsp_weight_moments(blk)
+    tot = parallel.sharded_weight_moments(blk, n).cpu().numpy()
+    assert (float(tot[0]), float(tot[1])) == (wm.sum_w, wm.sum_w2)
+    got = parallel.sharded_integrate(hk.identity(), spec, mother, n, hk.RngKey(1, 1), m12sq_builder)
+    want = hk.phsp_integrate(hk.identity(), spec, mother, n, hk.RngKey(1, 1), m12sq_builder)
+    assert (got.value, got.error) == (want.value, want.error)
+    with pytest.raises(ValueError, match="empty"):
+        parallel.sharded_integrate(hk.identity(), spec, mother, 0, hk.RngKey(1, 1), m12sq_builder)
+    small = hk.phsp_generate(spec, mother, 10, hk.RngKey(1, 1))
+    before = hk.phsp_weight_moments(small)
+    small.push([2.5] + [0.0] * 12)
+    after = hk.phsp_weight_moments(small)
+    assert after.n == 11 and after.sum_w == pytest.approx(before.sum_w + 2.5, rel=1e-15)
 
 
 @pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 10_001, 123_457])
