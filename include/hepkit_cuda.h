@@ -181,6 +181,14 @@ int hk_rng_raw64(const hk_key_t* key, const uint64_t* d_counters, int64_t n, uin
 int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, double* d_out,
                    void* stream);
 
+/* Raw Philox4x32-10 (Salmon et al., SC'11; Random123 philox4x32, R = 10), the
+ * round function of the production stream: row i of d_ctr_key is
+ * (ctr0..ctr3, key0, key1) as uint32, row i of d_out the 4 output words.  For
+ * known-answer tests of the device implementation.  The production stream
+ * maps draw j of event e (key.counter added) to words 2(j & 1), 2(j & 1) + 1
+ * of block ctr = (e lo, e hi, j >> 1, 0x686b7068), key = base(seed, stream). */
+int hk_philox4x32_10(const uint32_t* d_ctr_key, int64_t n, uint32_t* d_out, void* stream);
+
 /* ------------------------------------------------------------- generation */
 /* phsp_generate (phasespace.py:162-188) for rows [ev_begin, ev_begin+ev_count):
  * writes 4n+1 columns, d_cols[0] = weight, d_cols[1+4j+c] = daughter j+1,

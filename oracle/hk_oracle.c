@@ -55,6 +55,65 @@ static inline double u01(uint64_t base, uint64_t c) {
   return (double)(hko_mix64(base + c * HKO_GOLDEN) >> 11) * kInv53;
 }
 
+/*
+ * Philox4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy
+ * as 1, 2, 3", SC'11; Random123 philox4x32 with R = 10): the production stream
+ * of the CUDA path (not a reference stream; north_star subsystem 2).  Round:
+ * (c0, c1, c2, c3) -> (hi(M1 c2) ^ c1 ^ k0, lo(M1 c2), hi(M0 c0) ^ c3 ^ k1,
+ * lo(M0 c0)), M0 = 0xD2511F53, M1 = 0xCD9E8D57; key bumped by the Weyl
+ * constants (0x9E3779B9, 0xBB67AE85) between rounds.  Pinned against the
+ * Random123 known-answer vectors in tests/test_oracle_golden.py.
+ */
+void hko_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* rows x (ctr[4], key[2]) -> rows x 4 words */
+void hko_philox_rows(const uint32_t* in6, int64_t n, uint32_t* out4) {
+  for (int64_t i = 0; i < n; ++i) hko_philox4x32_10(in6 + 6 * i, in6 + 6 * i + 4, out4 + 4 * i);
+}
+
+#define HKO_RNG_REFERENCE 0
+#define HKO_RNG_PHILOX 1
+#define HKO_PHILOX_TAG 0x686b7068u /* "hkph" */
+
+/* The CUDA path's Philox stream mapping (csrc/hk_device.cuh draw_bits): draw
+ * j of event ev (key counter included) is word pair j & 1 of the block
+ * philox(ctr = (ev lo, ev hi, j >> 1, tag), key = (base lo, base hi)). */
+static inline uint64_t philox_bits(uint64_t base, uint64_t ev, uint64_t j) {
+  uint32_t ctr[4] = {(uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)(j >> 1), HKO_PHILOX_TAG};
+  uint32_t key[2] = {(uint32_t)base, (uint32_t)(base >> 32)}, o[4];
+  hko_philox4x32_10(ctr, key, o);
+  return (j & 1) ? (((uint64_t)o[2] << 32) | o[3]) : (((uint64_t)o[0] << 32) | o[1]);
+}
+
+/* uniform draw j of event evk (= event + key.counter) with D draws per event */
+typedef struct {
+  int mode;
+  uint64_t base;
+} rng_t;
+
+static inline double draw(const rng_t* r, uint64_t evk, uint64_t D, uint64_t j) {
+  if (r->mode == HKO_RNG_PHILOX) return (double)(philox_bits(r->base, evk, j) >> 11) * kInv53;
+  return u01(r->base, evk * D + j);
+}
+
+/* raw64 in the Philox mode (hk_rng_raw64): counter c -> block (c lo, c hi, 0, tag), words 0-1 */
+void hko_philox_raw64(uint64_t base, uint64_t kc, const uint64_t* counters, int64_t n, uint64_t* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = philox_bits(base, counters[i] + kc, 0);
+}
+
 /* raw64(key, counters): out[i] = mix(base + (counters[i] + kc) * G) */
 void hko_raw64(uint64_t base, uint64_t kc, const uint64_t* counters, int64_t n,
                uint64_t* out) {
@@ -101,12 +160,13 @@ static inline void apply_frame(const frame_t* f, double* v /* e,px,py,pz */) {
 
 /* One event in the rest frame: returns weight, fills p[4*n]. */
 static double rest_frame_event(int n, const double* m, double T, const double* csum,
-                               uint64_t base, uint64_t c0, double* p) {
+                               const rng_t* rng, uint64_t evk, double* p) {
+  const uint64_t D = (uint64_t)(3 * n - 4);
   double rno[HKO_MAXN], inv[HKO_MAXN], ps[HKO_MAXN];
   rno[0] = 0.0;
   rno[n - 1] = 1.0;
   for (int j = 0; j < n - 2; ++j) {  /* insertion sort == np.sort order */
-    double u = u01(base, c0 + (uint64_t)j);
+    double u = draw(rng, evk, D, (uint64_t)j);
     int i = j;
     while (i > 0 && rno[i] > u) {
       rno[i + 1] = rno[i];
@@ -124,9 +184,9 @@ static double rest_frame_event(int n, const double* m, double T, const double* c
   p[0] = m[0];
   for (int k = 1; k < n; ++k) {
     double q = ps[k];
-    uint64_t ca = c0 + (uint64_t)(n - 2 + 2 * (k - 1));
-    double cz = 2.0 * u01(base, ca) - 1.0;
-    double phi = kTwoPi * u01(base, ca + 1);
+    uint64_t ca = (uint64_t)(n - 2 + 2 * (k - 1));
+    double cz = 2.0 * draw(rng, evk, D, ca) - 1.0;
+    double phi = kTwoPi * draw(rng, evk, D, ca + 1);
     double s2 = 1.0 - cz * cz;
     double sz = sqrt(max0(s2));
     double nx = sz * cos(phi), ny = sz * sin(phi), nz = cz;
@@ -194,7 +254,8 @@ typedef struct {
   const double *masses, *csum;
   double T;
   frame_t mf;
-  uint64_t base, kc, ev_begin, D;
+  rng_t rng;
+  uint64_t kc, ev_begin;
   double* const* cols;
 } gen_ctx_t;
 
@@ -203,7 +264,7 @@ static void gen_body(void* vctx, int64_t lo, int64_t hi) {
   double p[4 * HKO_MAXN];
   for (int64_t i = lo; i < hi; ++i) {
     uint64_t ev = c->ev_begin + (uint64_t)i;
-    double w = rest_frame_event(c->n, c->masses, c->T, c->csum, c->base, (ev + c->kc) * c->D, p);
+    double w = rest_frame_event(c->n, c->masses, c->T, c->csum, &c->rng, ev + c->kc, p);
     if (c->moving)
       for (int j = 0; j < c->n; ++j) apply_frame(&c->mf, p + 4 * j);
     c->cols[0][i] = w;
@@ -213,12 +274,13 @@ static void gen_body(void* vctx, int64_t lo, int64_t hi) {
 
 int hko_generate(int n, const double* masses, double T, const double* csum, int moving,
                  const double* mother, double m_mother, uint64_t base, uint64_t kc,
-                 uint64_t ev_begin, int64_t ev_count, double* const* cols, int threads) {
+                 uint64_t ev_begin, int64_t ev_count, double* const* cols, int threads,
+                 int rng_mode) {
   if (n < 2 || n > HKO_MAXN) return 1;
   gen_ctx_t c;
   c.n = n; c.moving = moving; c.masses = masses; c.csum = csum; c.T = T;
   if (moving) c.mf = make_frame(mother[0], mother[1], mother[2], mother[3], m_mother);
-  c.base = base; c.kc = kc; c.ev_begin = ev_begin; c.D = (uint64_t)(3 * n - 4);
+  c.rng.mode = rng_mode; c.rng.base = base; c.kc = kc; c.ev_begin = ev_begin;
   c.cols = cols;
   hko_parallel_for(ev_count, threads, gen_body, &c);
   return 0;
@@ -236,7 +298,8 @@ typedef struct {
   int n_sub;
   const double *sub_masses, *csum;
   double T;
-  uint64_t base, kc, ev_begin, D;
+  rng_t rng;
+  uint64_t kc, ev_begin;
   double* out_w;
   double* const* out_cols;
 } chain_ctx_t;
@@ -249,8 +312,7 @@ static void chain_body(void* vctx, int64_t lo, int64_t hi) {
     double fe = c->in_p4[0][i], fx = c->in_p4[1][i], fy = c->in_p4[2][i], fz = c->in_p4[3][i];
     double m2 = fe * fe - fx * fx - fy * fy - fz * fz;
     double fm = sqrt(max0(m2));
-    double w = rest_frame_event(c->n_sub, c->sub_masses, c->T, c->csum, c->base,
-                                (ev + c->kc) * c->D, p);
+    double w = rest_frame_event(c->n_sub, c->sub_masses, c->T, c->csum, &c->rng, ev + c->kc, p);
     frame_t f = make_frame(fe, fx, fy, fz, fm);
     for (int j = 0; j < c->n_sub; ++j) apply_frame(&f, p + 4 * j);
     c->out_w[i] = c->in_w[i] * w;
@@ -261,7 +323,7 @@ static void chain_body(void* vctx, int64_t lo, int64_t hi) {
 int64_t hko_decay_chain(const double* in_w, const double* const* in_p4, int n_sub,
                         const double* sub_masses, double M_sub, double T, const double* csum,
                         uint64_t base, uint64_t kc, uint64_t ev_begin, int64_t ev_count,
-                        double* out_w, double* const* out_cols, int threads) {
+                        double* out_w, double* const* out_cols, int threads, int rng_mode) {
   if (n_sub < 2 || n_sub > HKO_MAXN) return -2;
   const double tol = 1e-9 * (M_sub > 1e-6 ? M_sub : 1e-6);
   for (int64_t i = 0; i < ev_count; ++i) {
@@ -272,7 +334,7 @@ int64_t hko_decay_chain(const double* in_w, const double* const* in_p4, int n_su
   }
   chain_ctx_t c;
   c.in_w = in_w; c.in_p4 = in_p4; c.n_sub = n_sub; c.sub_masses = sub_masses; c.csum = csum;
-  c.T = T; c.base = base; c.kc = kc; c.ev_begin = ev_begin; c.D = (uint64_t)(3 * n_sub - 4);
+  c.T = T; c.rng.mode = rng_mode; c.rng.base = base; c.kc = kc; c.ev_begin = ev_begin;
   c.out_w = out_w; c.out_cols = out_cols;
   hko_parallel_for(ev_count, threads, chain_body, &c);
   return -1;

@@ -62,12 +62,16 @@ def lib():
         L.hko_generate.restype = ctypes.c_int
         L.hko_generate.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
                                    ctypes.c_int, ctypes.c_void_p, ctypes.c_double, _u64, _u64,
-                                   _u64, _i64, ctypes.c_void_p, ctypes.c_int]
+                                   _u64, _i64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.hko_decay_chain.restype = _i64
         L.hko_decay_chain.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                       ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_void_p, _u64, _u64, _u64, _i64, ctypes.c_void_p,
-                                      ctypes.c_void_p, ctypes.c_int]
+                                      ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.hko_philox_rows.restype = None
+        L.hko_philox_rows.argtypes = [ctypes.c_void_p, _i64, ctypes.c_void_p]
+        L.hko_philox_raw64.restype = None
+        L.hko_philox_raw64.argtypes = [_u64, _u64, ctypes.c_void_p, _i64, ctypes.c_void_p]
         L.hko_unweight_flags.restype = None
         L.hko_unweight_flags.argtypes = [ctypes.c_void_p, _i64, ctypes.c_double, _u64, _u64, _u64,
                                          ctypes.c_void_p]
@@ -97,6 +101,24 @@ def uniform(seed: int, stream: int, counter: int, counters) -> np.ndarray:
     return out
 
 
+def philox4x32_10(ctr, key) -> np.ndarray:
+    """Philox4x32-10 blocks: ctr (rows x 4 uint32), key (rows x 2 uint32) -> rows x 4."""
+    ctr = np.asarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    key = np.asarray(key, dtype=np.uint32).reshape(-1, 2)
+    rows = np.ascontiguousarray(np.concatenate([ctr, key], axis=1))
+    out = np.empty((rows.shape[0], 4), dtype=np.uint32)
+    lib().hko_philox_rows(rows.ctypes.data, rows.shape[0], out.ctypes.data)
+    return out
+
+
+def philox_raw64(seed: int, stream: int, counter: int, counters) -> np.ndarray:
+    """hk_rng_raw64 in Philox mode: counter c -> words 0-1 of block (c lo, c hi, 0, tag)."""
+    c = np.ascontiguousarray(counters, dtype=np.uint64)
+    out = np.empty(c.shape, dtype=np.uint64)
+    lib().hko_philox_raw64(base(seed, stream), u64(counter), c.ctypes.data, c.size, out.ctypes.data)
+    return out
+
+
 def schema(n: int) -> list[str]:
     names = ["weight"]
     for k in range(1, n + 1):
@@ -120,9 +142,13 @@ def invariant_mass(e: float, px: float, py: float, pz: float) -> float:
     return math.sqrt(max(0.0, m2))
 
 
+RNG_MODES = {"reference": 0, "philox": 1}
+
+
 def generate(masses, M, n_events, seed, stream, counter=0, mother=None, ev_begin=0,
-             threads=1) -> dict[str, np.ndarray]:
-    """Rows [ev_begin, ev_begin+n_events) of phsp_generate as a name->column dict."""
+             threads=1, rng: str = "reference") -> dict[str, np.ndarray]:
+    """Rows [ev_begin, ev_begin+n_events) of phsp_generate as a name->column dict
+    (rng="philox": the CUDA path's production stream, hko_philox4x32_10)."""
     m, T, csum = _mass_terms(masses, M)
     n = len(m)
     mother = (float(M), 0.0, 0.0, 0.0) if mother is None else tuple(float(v) for v in mother)
@@ -132,14 +158,14 @@ def generate(masses, M, n_events, seed, stream, counter=0, mother=None, ev_begin
     cols = [np.empty(n_events) for _ in range(4 * n + 1)]
     rc = lib().hko_generate(n, m.ctypes.data, T, csum.ctypes.data, int(moving), mom.ctypes.data,
                             m_mother, base(seed, stream), u64(counter), u64(ev_begin),
-                            int(n_events), _ptrs(cols), int(threads))
+                            int(n_events), _ptrs(cols), int(threads), RNG_MODES[rng])
     if rc != 0:
         raise ValueError(f"oracle generate failed rc={rc}")
     return dict(zip(schema(n), cols))
 
 
 def decay_chain(block: dict[str, np.ndarray], k: int, sub_masses, M_sub, seed, stream,
-                counter=0, ev_begin=0, threads=1) -> dict[str, np.ndarray]:
+                counter=0, ev_begin=0, threads=1, rng: str = "reference") -> dict[str, np.ndarray]:
     n_old = (len(block) - 1) // 4
     m, T, csum = _mass_terms(sub_masses, M_sub)
     n_sub = len(m)
@@ -150,7 +176,8 @@ def decay_chain(block: dict[str, np.ndarray], k: int, sub_masses, M_sub, seed, s
     out = [np.empty(nev) for _ in range(4 * n_sub)]
     bad = lib().hko_decay_chain(w_in.ctypes.data, _ptrs(p4), n_sub, m.ctypes.data, float(M_sub),
                                 T, csum.ctypes.data, base(seed, stream), u64(counter),
-                                u64(ev_begin), nev, out_w.ctypes.data, _ptrs(out), int(threads))
+                                u64(ev_begin), nev, out_w.ctypes.data, _ptrs(out), int(threads),
+                                RNG_MODES[rng])
     if bad >= 0:
         raise ValueError(f"event {bad}: daughter {k} mass does not match sub-decay mother mass")
     cols = [out_w]

@@ -43,7 +43,7 @@ EXPORTS = (
     "hk_set_jit_mode", "hk_jit_count", "hk_jit_source", "hk_jit_compile",
     "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles", "hk_fold_segments",
     "hk_init", "hk_shutdown", "hk_clique_size", "hk_allreduce_partials", "hk_allgather_partials",
-    "hk_fold_supers",
+    "hk_fold_supers", "hk_philox4x32_10",
 )
 
 
@@ -111,6 +111,7 @@ _SIGS = {
     "hk_num_chunks": (_I64, [_I64]),
     "hk_rng_raw64": (_INT, [_K, _P, _I64, _P, _P]),
     "hk_rng_uniform": (_INT, [_K, _P, _I64, _P, _P]),
+    "hk_philox4x32_10": (_INT, [_P, _I64, _P, _P]),
     "hk_phsp_generate": (_INT, [_D, _K, _U64, _I64, _PP, _P, _P]),
     "hk_phsp_generate_host": (_INT, [_D, _K, _U64, _I64, _PP, _PD, _P, ctypes.c_size_t, _P]),
     "hk_phsp_decay_chain": (_INT, [_P, _PP, _D, _K, _U64, _I64, _P, _PP, _P, _P]),

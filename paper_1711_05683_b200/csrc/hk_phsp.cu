@@ -578,6 +578,16 @@ __global__ void k_rng(RngParams rp, const uint64_t* ctr, int64_t n, uint64_t* ra
   if (uni) uni[i] = to_unit(bits);
 }
 
+// Raw Philox4x32-10 blocks on (ctr[4], key[2]) rows -- the same device round
+// function the production stream uses, exposed for known-answer tests.
+__global__ void k_philox_rows(const uint32_t* in6, int64_t n, uint32_t* out4) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* r = in6 + 6 * i;
+  const Philox4 o = philox4x32_10(r[0], r[1], r[2], r[3], r[4], r[5]);
+  for (int k = 0; k < 4; ++k) out4[4 * i + k] = o.v[k];
+}
+
 // ----------------------------------------------------------------- folds ---
 // Deterministic fold over one thread-block cluster of kFoldCtas CTAs: global
 // thread g sums parts g, g + 8192, ... in order, a fixed shuffle/smem tree
@@ -833,6 +843,14 @@ int hk_rng_raw64(const hk_key_t* key, const uint64_t* d_counters, int64_t n, uin
   k_rng<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(make_rng(*key), d_counters, n,
                                                                     d_out, nullptr);
   return check_launch("k_rng");
+}
+
+int hk_philox4x32_10(const uint32_t* d_ctr_key, int64_t n, uint32_t* d_out, void* stream) {
+  HK_REQUIRE(n >= 0, "negative n");
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_ctr_key && d_out, "NULL pointer");
+  k_philox_rows<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(d_ctr_key, n, d_out);
+  return check_launch("k_philox_rows");
 }
 
 int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, double* d_out,

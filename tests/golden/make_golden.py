@@ -31,6 +31,9 @@ from hepkit.rng import raw64, uniform_array, _base  # noqa: E402
 from hepkit.fitting import generate_model_sample  # noqa: E402
 import toymodel  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from generic_models import GENERIC_POINTS, generic_models  # noqa: E402
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 # pinned decay inputs (GeV)
@@ -74,6 +77,98 @@ def m12sq_builder(cols):
     pz = cols["p1_pz"] + cols["p2_pz"]
     return (e * e - px * px - py * py - pz * pz,)
 
+
+
+def _x(store) -> np.ndarray:
+    return np.asarray(store.column("x0"))
+
+
+def add_c4(arrays, scalars) -> None:
+    """The bench's FCN data set (config C4): build_model(scale=200),
+    generate_model_sample(RngKey(7, 2), poisson=False) -> 1e7 events.  Only
+    fingerprints are frozen (the full column is 80 MB): head, sum, a SHA-256
+    of the bytes, a strided sample, and nll at two points."""
+    import hashlib
+    from hepkit.fitting import _poisson_count
+
+    model = toymodel.build_model(scale=200)
+    data = generate_model_sample(model, hk.RngKey(7, 2), poisson=False, workers=8)
+    x = _x(data)
+    idx = np.arange(0, len(x), 99_991, dtype=np.int64)
+    arrays["c4_strided_idx"] = idx
+    arrays["c4_strided_x"] = x[idx]
+    c4 = {"n": len(x), "head": x[:8].tolist(), "xsum": float(np.sum(x)),
+          "sha256": hashlib.sha256(x.tobytes()).hexdigest(),
+          "nll_truth": hk.nll(model, data, ["x0"], workers=8)}
+    ps = model.param_set()
+    ps["mean"].set(4.9)
+    ps["sigma"].set(0.55)
+    ps["tau"].set(2.8)
+    c4["nll_alt"] = hk.nll(model, data, ["x0"], workers=8)
+    c4["alt_point"] = {"mean": 4.9, "sigma": 0.55, "tau": 2.8}
+    # Poisson component counts (fitting.py:519-523) for the same key and yields
+    c4["poisson_counts"] = [_poisson_count(y.value, hk.RngKey(7, 2), c)
+                            for c, (y, _) in enumerate(toymodel.build_model(scale=200).components)]
+    # a poisson=True toy at scale 0.2: count and bits
+    small = generate_model_sample(toymodel.build_model(scale=0.2), hk.RngKey(7, 2), poisson=True)
+    xs = _x(small)
+    arrays["c4_poisson_small_x"] = xs
+    c4["poisson_small_n"] = len(xs)
+    scalars["c4"] = c4
+
+
+def add_yields_splot(arrays, scalars, data) -> None:
+    """Reference yield-stationarity sums and sPlot outputs on the scale-0.2 toy
+    data (golden nll_x): at the truth, at an off-optimum point, and -- for
+    sPlot -- at the parameters of the reference's own fit."""
+    from hepkit.fitting import _yield_stationarity
+    from hepkit.splot import splot_matrix, splot_weights
+
+    out = {"points": []}
+    for pt in ({}, {"mean": 5.1, "sigma": 0.45, "tau": 3.3, "n_sig": 3900.0, "n_bkg": 6200.0}):
+        m = toymodel.build_model(scale=0.2, **pt)
+        g, A = _yield_stationarity(m, data, ["x0"], 1)
+        out["points"].append({"values": {p.name: p.value for p in m.param_set()},
+                              "g": g.tolist(), "A": A.tolist()})
+    m = toymodel.build_model(scale=0.2)
+    res = hk.fit(m, data, ["x0"])
+    V = splot_matrix(m, data, ["x0"])
+    sw = splot_weights(m, data, ["x0"], V)
+    out["fit_values"] = {p.name: p.value for p in m.param_set()}
+    out["fit_status"] = res.status.value
+    out["V"] = V.tolist()
+    arrays["splot_sw"] = np.stack([np.asarray(sw.column(n)) for n in sw.schema.names])
+    scalars["yields_splot"] = out
+
+
+def add_generic_models(arrays, scalars) -> None:
+    rs = np.random.default_rng(20251018)
+    n = 3 * 4096 + 17
+    # G1 data on [0.6, 1.2]: a Cauchy peak + uniform
+    xb = rs.standard_cauchy(n) * 0.0237 + 0.8955
+    xb = np.where((xb > 0.6) & (xb < 1.2), xb, rs.uniform(0.6, 1.2, n))
+    arrays["g1_x"] = xb
+    # G2 data on [0, 10]^2
+    arrays["g2_x"] = np.clip(rs.normal(5.0, 0.8, n), 0.01, 9.99)
+    arrays["g2_y"] = np.clip(rs.exponential(2.5, n), 0.01, 9.99)
+    # G6 data on [0, 10]
+    arrays["g6_x"] = np.clip(np.concatenate([rs.normal(mu, s, n // 6) for mu, s in
+                                             ((2.0, 0.3), (4.0, 0.5), (6.0, 0.4), (8.0, 0.6))]
+                                            + [rs.exponential(3.0, n // 6), rs.uniform(0, 10, n - 5 * (n // 6))]),
+                             0.01, 9.99)
+    s1 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g1_x"]])
+    s2 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0", "x1"), [arrays["g2_x"], arrays["g2_y"]])
+    s6 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g6_x"]])
+    out = {"points": GENERIC_POINTS, "g1": [], "g2": [], "g6": [], "g6_yields": []}
+    from hepkit.fitting import _yield_stationarity
+    for pt in GENERIC_POINTS:
+        ms = generic_models(hk, np, pt)
+        out["g1"].append(hk.nll(ms["g1"], s1, ["x0"]))
+        out["g2"].append(hk.nll(ms["g2"], s2, ["x0", "x1"]))
+        out["g6"].append(hk.nll(ms["g6"], s6, ["x0"]))
+        g, A = _yield_stationarity(ms["g6"], s6, ["x0"], 1)
+        out["g6_yields"].append({"g": g.tolist(), "A": A.tolist()})
+    scalars["generic"] = out
 
 def main() -> None:
     arrays: dict[str, np.ndarray] = {}
@@ -211,6 +306,13 @@ def main() -> None:
         "breakup_2_05_03": hk.breakup_momentum(2.0, 0.5, 0.3),
         "max_weight_b0": hk.phsp_max_weight(spec_b0),
     }
+
+    # ---- C4 data set pins (cli.py:321-323) ---------
+    add_c4(arrays, scalars)
+    # ---- yield stationarity + sPlot (fitting.py:401-434, splot.py:45-117) --
+    add_yields_splot(arrays, scalars, data)
+    # ---- FCN of generic shapes / observable arity 2 (fitting.py:160-199) ---
+    add_generic_models(arrays, scalars)
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:

@@ -119,3 +119,45 @@ def test_window_property(oracle):
 def test_average_builder_matches_oracle_pair_mass(oracle):
     c = oracle.generate(B0_DAUGHTERS, B0_MASS, 5000, 4, 1)
     assert np.array_equal(m12sq_builder(c)[0], oracle.pair_mass2(c, 1, 2))
+
+
+# Random123 known-answer vectors for philox4x32 with R = 10 rounds (Random123
+# distribution, examples/kat_vectors: ctr[4] key[2] -> out[4]).  They pin the
+# oracle's Philox restatement, which in turn is the checker for the device's
+# production stream (tests/test_parity_pins_gpu.py).
+PHILOX_KAT = [
+    ((0x00000000, 0x00000000, 0x00000000, 0x00000000), (0x00000000, 0x00000000),
+     (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+    ((0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF), (0xFFFFFFFF, 0xFFFFFFFF),
+     (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+]
+
+
+def test_oracle_philox_known_answers(oracle):
+    got = oracle.philox4x32_10([c for c, _, _ in PHILOX_KAT], [k for _, k, _ in PHILOX_KAT])
+    assert got.tolist() == [list(o) for _, _, o in PHILOX_KAT]
+
+
+def test_oracle_philox_stream_mapping(oracle):
+    """The production stream's draw layout (hk_device.cuh draw_bits) from the
+    raw blocks: event e's raw64 in Philox mode is words (0, 1) of block
+    (e lo, e hi, 0, "hkph") under key base(seed, stream)."""
+    seed, stream, kc = 7, 1, 5
+    ctr = np.array([0, 1, 2**32 + 3, 2**63 + 11], dtype=np.uint64)
+    b = oracle.base(seed, stream)
+    ev = ctr + np.uint64(kc)
+    blocks = oracle.philox4x32_10(
+        np.stack([ev & np.uint64(0xFFFFFFFF), ev >> np.uint64(32), np.zeros_like(ev),
+                  np.full_like(ev, 0x686B7068)], axis=1),
+        np.tile(np.array([b & 0xFFFFFFFF, b >> 32], dtype=np.uint64), (len(ev), 1)))
+    want = (blocks[:, 0].astype(np.uint64) << np.uint64(32)) | blocks[:, 1].astype(np.uint64)
+    assert np.array_equal(oracle.philox_raw64(seed, stream, kc, ctr), want)
+    # a Philox-mode generation is a valid phase-space sample: conservation at rest
+    cols = oracle.generate(B0_DAUGHTERS, B0_MASS, 2000, 1, 1, rng="philox")
+    e = sum(cols[f"p{j}_e"] for j in (1, 2, 3))
+    px = sum(cols[f"p{j}_px"] for j in (1, 2, 3))
+    assert np.allclose(e, B0_MASS, rtol=1e-13) and np.allclose(px, 0.0, atol=1e-13)
+    ref = oracle.generate(B0_DAUGHTERS, B0_MASS, 2000, 1, 1)
+    assert not np.array_equal(cols["weight"], ref["weight"])
