@@ -46,8 +46,8 @@ extern "C" {
 #define HK_CHUNK 4096        /* rows per reduction partial (parallel.py:18) */
 #define HK_WARP_SLICES 8     /* per-warp weight partials per chunk (generation kernels) */
 #define HK_MAX_DAUGHTERS 16  /* templated fast path covers n <= 8 */
-#define HK_MAX_PROGRAM 48    /* ops per device functor program */
-#define HK_MAX_SLOTS 16      /* virtual registers per program */
+#define HK_MAX_PROGRAM 256   /* ops per device functor program */
+#define HK_MAX_SLOTS 32      /* virtual registers per program */
 #define HK_MAX_COMPONENTS 8  /* p.d.f. components per extended model */
 #define HK_NO_BAD_ROW UINT64_MAX
 
@@ -89,7 +89,7 @@ enum hk_opcode {
   HK_OP_ADD = 2,    /* dst = a + b */
   HK_OP_SUB = 3,    /* dst = a - b */
   HK_OP_MUL = 4,    /* dst = a * b */
-  HK_OP_DIV = 5,    /* dst = a / b; b == 0 is a domain error (functors.py:200-207) */
+  HK_OP_DIV = 5,    /* dst = a / b; b == 0 is a domain error (_BinaryOp "/", functors.py:200-207) */
   HK_OP_NEG = 6,    /* dst = -a */
   HK_OP_SQRT = 7,   /* dst = sqrt(a) */
   HK_OP_EXP = 8,    /* dst = exp(a) */
@@ -98,7 +98,9 @@ enum hk_opcode {
   HK_OP_EXPO = 11,  /* dst = exp(-a / cst[i]) (functors.py:157-161) */
   HK_OP_BW = 12,    /* dst = 1/((a - m0^2)^2 + m0^2 g0^2), m0=cst[i], g0=cst2[i] */
   HK_OP_ADD0 = 13,  /* dst = a + 0.0 (Coordinate, functors.py:248-249) */
-  HK_OP_SQUARE = 14 /* dst = a * a */
+  HK_OP_SQUARE = 14, /* dst = a * a */
+  HK_OP_UDIV = 15    /* dst = a / b, unchecked: numpy division inside a traced closure or
+                        arg_builder, or a shape body (IEEE inf/nan, no EvaluationError) */
 };
 
 typedef struct hk_program {
@@ -313,7 +315,7 @@ int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chu
                    int64_t n_chunks_local, int32_t recs_per_chunk, int32_t width, int32_t s_begin,
                    int32_t s_count, double* d_out, void* stream);
 
-/* Deterministic fold of n_parts partials of `width` (<= 32) doubles each
+/* Deterministic fold of n_parts partials of `width` (<= 72: K + K^2 for 8 components) doubles each
  * (parallel.py:86-92 semantics, fixed tree order) into d_out[width]. */
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,
                      void* stream);
@@ -328,6 +330,58 @@ int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, d
 int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                     uint64_t* d_first_bad, void* stream);
 
+/* The FCN of ANY traceable model (fitting.py:160-166 with any FunctorExpr
+ * shape -- closures, compositions, sums/products -- and any observable
+ * arity): the density is a lowered functor program whose constants (yields,
+ * host norms, shape parameters) sit in program.cst and change per call while
+ * the op structure stays fixed.  pdf_slot[k] holds pdf_k = shape_k / norm_k and
+ * program.result the density sum_k N_k pdf_k in the reference's order after the
+ * program runs; HK_OP_COL c reads observable column c. */
+#define HK_FCN_MAX_OBS 8
+typedef struct hk_density {
+  int32_t n_obs;  /* observable columns, 1..HK_FCN_MAX_OBS */
+  int32_t n_comp; /* components K, 1..HK_MAX_COMPONENTS */
+  int32_t pdf_slot[HK_MAX_COMPONENTS];
+  double yield[HK_MAX_COMPONENTS]; /* N_k (the ratio sums' density p @ N, fitting.py:416) */
+  hk_program_t program;
+} hk_density_t;
+
+/* hk_nll_eval for an hk_density_t over d_obs[n_obs] columns: same workspace,
+ * schedule and fold; *h_first_div0 = first row with a zero divisor
+ * (functors.py:200-207) or HK_NO_BAD_ROW.  The program runs through the
+ * interpreter or, per the hk_set_jit_mode policy, an NVRTC-specialised kernel
+ * compiled once per op structure (constants stay kernel arguments). */
+int hk_nll_program_eval(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                        double* d_work, double* h_logsum, uint64_t* h_first_bad,
+                        uint64_t* h_first_div0, void* stream);
+
+/* Both FCN entry points are asynchronous when h_logsum is NULL: the result
+ * stays on the device in d_work[0] (sum of logs), d_work[1] (first bad row,
+ * u64 bits) and d_work[5] (first zero divisor, u64 bits).  That is the
+ * row-sharded multi-GPU FCN's step 1; step 2 all-gathers d_work[0..7] of every
+ * rank (the caller stores its shard's first global row as a double in
+ * d_work[6]) with one stream-ordered NCCL collective, and step 3 is: */
+
+/* Rank-order fold of world gathered 8-double FCN records (d_gathered[8 r ..]):
+ * *h_logsum = sum over r in order of [0]; *h_first_bad / *h_first_div0 = the
+ * smallest global row ([6] + local row) over ranks, or HK_NO_BAD_ROW.  One
+ * kernel that publishes into the mapped mailbox: the sharded FCN has a single
+ * host synchronisation per evaluation.  Synchronous. */
+int hk_nll_combine(const double* d_gathered, int32_t world, double* h_logsum, uint64_t* h_first_bad,
+                   uint64_t* h_first_div0, void* stream);
+
+/* Yield-stationarity / sPlot sums for an hk_density_t (any shape, K <= 8):
+ * per chunk K values sum_e r_k and K*K values sum_e r_k r_j, r_k = pdf_k / d,
+ * d = sum_k N_k pdf_k; d_first_bad[0]: d not > 0; [1]: d not > 0 or
+ * non-finite; [2]: first zero divisor (all initialised to HK_NO_BAD_ROW). */
+int hk_ratio_partials_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                              double* d_partials, uint64_t* d_first_bad, void* stream);
+
+/* sWeights for an hk_density_t (K <= 8): d_out[s][i] = sum_j V[s*K+j] pdf_j / d. */
+int hk_splot_weights_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                             const double* V, double* const* d_out, uint64_t* d_first_bad,
+                             void* stream);
+
 /* One FCN evaluation end to end.  Synchronous.  *h_logsum = sum_e ln density;
  * *h_first_bad = first failing row or HK_NO_BAD_ROW.  One kernel launch (the
  * last CTA folds the tile partials in a fixed order and publishes the result
@@ -338,7 +392,8 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
  * the sum's grouping (not its value beyond rounding) depends on the SM count. */
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
-/* workspace size of hk_nll_eval for n rows (4 + one partial per scheduled CTA) */
+/* workspace size of hk_nll_eval / hk_nll_program_eval for n rows (8 + one
+ * partial per scheduled CTA) */
 int64_t hk_nll_work_doubles(int64_t n);
 
 /* Yield-stationarity sums (fitting.py:401-434) and the sWeights matrix

@@ -20,8 +20,8 @@ LIB_PATH = os.environ.get("HK_LIB_PATH") or os.path.join(HERE, "libhepkit_cuda.s
 HK_OK, HK_EINVAL, HK_ECUDA, HK_EDOMAIN, HK_EUNSUPPORTED = 0, 1, 2, 3, 4
 HK_CHUNK = 4096
 HK_MAX_DAUGHTERS = 16
-HK_MAX_PROGRAM = 48
-HK_MAX_SLOTS = 16
+HK_MAX_PROGRAM = 256
+HK_MAX_SLOTS = 32
 HK_MAX_COMPONENTS = 8
 HK_NO_BAD_ROW = (1 << 64) - 1
 HK_RNG_REFERENCE, HK_RNG_PHILOX = 0, 1
@@ -29,7 +29,7 @@ HK_SHAPE_GAUSS, HK_SHAPE_EXPO = 0, 1
 
 # opcodes (enum hk_opcode)
 OP_COL, OP_CONST, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_NEG, OP_SQRT, OP_EXP, OP_LOG = range(10)
-OP_GAUSS, OP_EXPO, OP_BW, OP_ADD0, OP_SQUARE = range(10, 15)
+OP_GAUSS, OP_EXPO, OP_BW, OP_ADD0, OP_SQUARE, OP_UDIV = range(10, 16)
 
 # symbols the header declares; tests check the .so exports every one
 EXPORTS = (
@@ -44,6 +44,7 @@ EXPORTS = (
     "hk_csv_scratch_bytes", "hk_format_csv", "hk_nll_work_doubles", "hk_fold_segments",
     "hk_init", "hk_shutdown", "hk_clique_size", "hk_allreduce_partials", "hk_allgather_partials",
     "hk_fold_supers", "hk_philox4x32_10",
+    "hk_nll_program_eval", "hk_ratio_partials_program", "hk_splot_weights_program", "hk_nll_combine",
 )
 
 
@@ -84,6 +85,16 @@ class hk_model_t(ctypes.Structure):
                 ("p1", ctypes.c_double * HK_MAX_COMPONENTS)]
 
 
+HK_FCN_MAX_OBS = 8
+
+
+class hk_density_t(ctypes.Structure):
+    _fields_ = [("n_obs", ctypes.c_int32), ("n_comp", ctypes.c_int32),
+                ("pdf_slot", ctypes.c_int32 * HK_MAX_COMPONENTS),
+                ("yield_", ctypes.c_double * HK_MAX_COMPONENTS),
+                ("program", hk_program_t)]
+
+
 HK_PAIR_NONE, HK_PAIR_MASS2, HK_PAIR_BW = 0, 1, 2
 
 
@@ -100,6 +111,7 @@ _D = ctypes.POINTER(hk_decay_t)      # structs: ctypes passes byref automaticall
 _K = ctypes.POINTER(hk_key_t)
 _F = ctypes.POINTER(hk_program_t)
 _M = ctypes.POINTER(hk_model_t)
+_DM = ctypes.POINTER(hk_density_t)
 _PP = ctypes.POINTER(ctypes.c_void_p)  # double* const* column-pointer arrays
 _PD = ctypes.POINTER(ctypes.c_double)  # host doubles
 _PU = ctypes.POINTER(ctypes.c_uint64)  # host u64
@@ -122,6 +134,10 @@ _SIGS = {
     "hk_fold_partials": (_INT, [_P, _I64, _I32, _P, _P]),
     "hk_nll_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
     "hk_nll_eval": (_INT, [_P, _I64, _M, _P, _PD, _PU, _P]),
+    "hk_nll_program_eval": (_INT, [_PP, _I64, _DM, _P, _PD, _PU, _PU, _P]),
+    "hk_ratio_partials_program": (_INT, [_PP, _I64, _DM, _P, _P, _P]),
+    "hk_nll_combine": (_INT, [_P, _I32, _PD, _PU, _PU, _P]),
+    "hk_splot_weights_program": (_INT, [_PP, _I64, _DM, _PD, _PP, _P, _P]),
     "hk_model_density": (_INT, [_P, _I64, _M, _P, _P]),
     "hk_yield_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),
     "hk_splot_weights": (_INT, [_P, _I64, _M, _PD, _PP, _P, _P]),

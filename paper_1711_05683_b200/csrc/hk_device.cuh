@@ -615,9 +615,11 @@ __device__ __forceinline__ void record_bad(unsigned long long* first_bad, uint64
 // Every thread runs the same op stream, so the switch is warp-uniform.
 // `load(c)` supplies column c of the current event.  Division by zero sets
 // *div0 (functors.py:200-207 raises before evaluating).
+// run_program_into leaves every slot in r (multi-output programs keep their
+// outputs in pinned slots, functors.compile_program(keep=...)).
 template <class Load>
-__device__ __forceinline__ double run_program(const hk_program_t& P, Load load, bool* div0) {
-  double r[HK_MAX_SLOTS];
+__device__ __forceinline__ void run_program_into(const hk_program_t& P, Load load, bool* div0,
+                                                 double (&r)[HK_MAX_SLOTS]) {
   for (int i = 0; i < P.n_ops; ++i) {
     const int op = P.op[i];
     double v;
@@ -652,10 +654,17 @@ __device__ __forceinline__ double run_program(const hk_program_t& P, Load load, 
       }
       case HK_OP_ADD0: v = r[P.a[i]] + 0.0; break;
       case HK_OP_SQUARE: v = r[P.a[i]] * r[P.a[i]]; break;
+      case HK_OP_UDIV: v = r[P.a[i]] / r[P.b[i]]; break;
       default: v = __longlong_as_double(0x7ff8000000000000ll); break;
     }
     r[P.dst[i]] = v;
   }
+}
+
+template <class Load>
+__device__ __forceinline__ double run_program(const hk_program_t& P, Load load, bool* div0) {
+  double r[HK_MAX_SLOTS];
+  run_program_into(P, load, div0, r);
   return r[P.result];
 }
 

@@ -14,11 +14,13 @@
 // usually L2-resident (1e7 events = 80 MB < 126 MB L2).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 
 #include "hepkit_cuda.h"
 #include "hk_device.cuh"
+#include "hk_fcn.cuh"
 #include "hk_host.h"
 
 namespace hk {
@@ -91,56 +93,6 @@ __device__ __forceinline__ bool density_factored(const Coeffs& c, double x, doub
   return *M > c.m_lo && *M < c.m_hi;
 }
 
-// sum_e ln d_e as ln(prod_e d_e), the product kept as a mantissa in [1, 2^16)
-// and an integer binary exponent: one log per 16 events instead of 16, the
-// exponent bookkeeping on the integer pipe.  Each product step rounds once
-// (<= 2^-53 relative), the same order of error as the per-event logs the
-// reference sums; far inside the 1e-10 FCN tolerance.
-struct LogProd {
-  double m = 1.0;
-  int e = 0;
-
-  __device__ __forceinline__ void add(double d) {
-    long long b = __double_as_longlong(d);
-    int ex = (int)((b >> 52) & 0x7ff);
-    if (ex == 0) {  // subnormal (or zero, which the caller flags as bad)
-      b = __double_as_longlong(d * 18014398509481984.0);  // * 2^54
-      ex = (int)((b >> 52) & 0x7ff) - 54;
-    }
-    e += ex - 1023;
-    m *= __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-  }
-
-  // add() for a value known to be a normal double (the factored density's s):
-  // no subnormal check, same result
-  __device__ __forceinline__ void add_normal(double d) {
-    const long long b = __double_as_longlong(d);
-    e += (int)((b >> 52) & 0x7ff) - 1023;
-    m *= __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-  }
-
-  // move m's binary exponent into e (exact): keeps m in [1, 2) so a thread
-  // can multiply any number of events with one log at the end
-  __device__ __forceinline__ void renorm() {
-    const long long b = __double_as_longlong(m);
-    e += (int)((b >> 52) & 0x7ff) - 1023;
-    m = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
-  }
-
-  __device__ __forceinline__ double value() const {
-    const double ln2_hi = 6.93147180369123816490e-01;  // 32 significant bits: e * ln2_hi is exact
-    const double ln2_lo = 1.90821492927058770002e-10;
-    return (e * ln2_hi + log(m)) + e * ln2_lo;
-  }
-};
-
-// FCN tiles of HK_FCN_TILE = 4096 rows (16 per thread, one log per 16
-// events).  2048-row tiles (8.25 waves instead of 4.1 for 1e7 events, less
-// tail) measured slower on B200 -- 38.3 vs 36.0 us per kernel -- because the
-// extra logs cost more than the tail they remove.
-constexpr int kFcnTile = HK_FCN_TILE;
-constexpr int kFcnRows = kFcnTile / kBlock;
-
 // One tile: returns sum ln d over this thread's rows; flags
 // d <= 0 / non-finite (fitting.py:200-205) as ~row in *bad (max = first row).
 template <int V>
@@ -205,38 +157,6 @@ __global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, in
   }
 }
 
-// One-launch FCN: the same event pass, then the last CTA to finish folds all
-// chunk partials in a fixed order (deterministic whichever CTA is last),
-// publishes (sum, first bad row) and re-arms the workspace for the next call.
-// The first-bad cell holds ~row under atomicMax so that an all-zero
-// workspace means "no bad row".
-struct FcnWork {
-  double* out;               // [0] sum of logs, [1] first bad row (u64 bits)
-  unsigned long long* bad;   // ~row of the first non-positive density, 0 = none
-  unsigned int* ticket;      // CTAs finished
-  double* part;              // one partial per chunk
-  // optional zero-copy publication into mapped pinned host memory:
-  // host_mail[1..2] = out[0..1], then host_mail[0] = seq (after a system fence)
-  volatile unsigned long long* host_mail;
-  unsigned long long seq;
-  // tile schedule (fcn_schedule): CTA b < full owns tile b (4096 rows); the
-  // rows from full * 4096 on are split evenly over tail_ctas more CTAs, so
-  // the last wave is short instead of a few full tiles on an idle GPU
-  int64_t full, tail_ctas;
-};
-
-__device__ __forceinline__ void fcn_range(const FcnWork& w, int64_t n, int64_t b, int64_t* begin,
-                                          int64_t* end) {
-  if (b < w.full) {
-    *begin = b * kFcnTile;
-    *end = *begin + kFcnTile;
-    return;
-  }
-  const int64_t t0 = w.full * kFcnTile, rem = n - t0, j = b - w.full;
-  *begin = t0 + rem * j / w.tail_ctas;
-  *end = t0 + rem * (j + 1) / w.tail_ctas;
-}
-
 // 4 CTAs/SM (64 registers) measured best for the one-launch FCN on B200:
 // C-ABI call 47.8 us; 5 CTAs (48 regs + spills) 50.6, 6 CTAs 53.9, 8 CTAs 64.4,
 // and an unconstrained (256, 1) bound lets ptxas take 216 registers (82 us).
@@ -259,31 +179,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const d
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
-  // block_sum_store's writer is thread 0: it alone fences before the ticket
-  __shared__ unsigned int s_ticket;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_ticket = atomicAdd(w.ticket, 1u);
-  }
-  __syncthreads();
-  if (s_ticket != gridDim.x - 1) return;
-  __threadfence();
-  double acc[1] = {0.0};
-  for (int64_t i = threadIdx.x; i < chunks; i += kBlock) acc[0] += __ldcg(w.part + i);
-  __shared__ double total;
-  block_sum_store<1>(acc, &total);
-  if (threadIdx.x == 0) {
-    const unsigned long long b = atomicExch(w.bad, 0ull);
-    w.out[0] = total;
-    w.out[1] = __longlong_as_double((long long)~b);
-    *w.ticket = 0u;
-    if (w.host_mail) {
-      w.host_mail[1] = (unsigned long long)__double_as_longlong(total);
-      w.host_mail[2] = ~b;
-      __threadfence_system();
-      w.host_mail[0] = w.seq;
-    }
-  }
+  fcn_finish(w, chunks);
 }
 
 // Reference op order (fitting.py:160-166, functors.py:142-143, :161) with no
@@ -544,6 +440,206 @@ void fcn_schedule(int64_t n, int64_t* full, int64_t* tail_ctas) {
   *tail_ctas = rem == 0 ? 0 : (want < slots ? want : slots);
 }
 
+// d_work layout of the one-launch FCN (zero-filled once by the caller,
+// re-armed by the kernel): [0] sum of logs, [1] first bad row (u64 bits),
+// [2] ~bad-row cell, [3] CTA ticket, [4] ~zero-divisor cell, [5] first zero
+// divisor row (u64 bits), [6..7] caller's (hk_nll_combine: [6] = the shard's
+// first global row), [8..] partials.
+constexpr int kFcnWorkHead = 8;
+
+// mb == NULL: asynchronous call, the result stays in d_work[0, 1, 5]
+int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
+  w->out = d_work;
+  w->bad = reinterpret_cast<unsigned long long*>(d_work + 2);
+  w->ticket = reinterpret_cast<unsigned int*>(d_work + 3);
+  w->div0 = reinterpret_cast<unsigned long long*>(d_work + 4);
+  w->part = d_work + kFcnWorkHead;
+  w->host_mail = nullptr;
+  w->seq = 0;
+  if (mb) {
+    if (int rc = mailbox(mb)) return rc;
+    w->host_mail = (*mb)->d;
+    w->seq = ++(*mb)->seq;
+  }
+  fcn_schedule(n, &w->full, &w->tail_ctas);
+  return HK_OK;
+}
+
+// Rank-order fold of gathered FCN results (hk_nll_combine): one thread.
+__global__ void k_nll_combine(const double* g, int world, FcnWork w) {
+  if (threadIdx.x != 0) return;
+  double total = 0.0;
+  unsigned long long bad = ~0ull, zero = ~0ull;
+  for (int r = 0; r < world; ++r) {
+    const double* v = g + 8 * r;
+    total += v[0];
+    const unsigned long long off = (unsigned long long)v[6];
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[1]);
+    const unsigned long long z = (unsigned long long)__double_as_longlong(v[5]);
+    if (b != ~0ull && off + b < bad) bad = off + b;
+    if (z != ~0ull && off + z < zero) zero = off + z;
+  }
+  w.host_mail[1] = (unsigned long long)__double_as_longlong(total);
+  w.host_mail[2] = bad;
+  w.host_mail[3] = zero;
+  __threadfence_system();
+  w.host_mail[0] = w.seq;
+}
+
+// The last CTA writes the result into mapped host memory and then the
+// sequence number; spin on it (no memcpy, no stream sync on the fast path).
+// Every 4096 polls the stream is queried so a faulted kernel cannot hang us.
+int fcn_wait(Mailbox* mb, unsigned long long seq, cudaStream_t st, const char* what,
+             double* h_logsum, uint64_t* h_first_bad, uint64_t* h_first_div0) {
+  for (unsigned spins = 1;; ++spins) {
+    if (mb->h[0] == seq) break;
+    if ((spins & 4095u) == 0) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) {
+        if (mb->h[0] == seq) break;
+        set_error("%s: kernel finished without publishing its result", what);
+        return HK_ECUDA;
+      }
+      if (q != cudaErrorNotReady) return cuda_fail(q, what);
+    }
+  }
+  // the device fenced (system scope) before writing seq; order our reads
+  // of the payload after the seq read (weakly ordered hosts, e.g. Grace)
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const unsigned long long sum_bits = mb->h[1];
+  std::memcpy(h_logsum, &sum_bits, sizeof(double));
+  *h_first_bad = mb->h[2];
+  if (h_first_div0) *h_first_div0 = mb->h[3];
+  return HK_OK;
+}
+
+// ------------------------------------------------ program-driven models ---
+// The density of any lowered model (hk_density_t) through the interpreter;
+// hk_jit.cu specialises the same pass per op structure.
+__global__ void __launch_bounds__(kBlock) k_nll_program(const __grid_constant__ FcnProgArgs a) {
+  const auto dens = [&](int64_t r, bool& z) -> double {
+    return run_program(a.prog, [&](int c) { return __ldg(a.cols[c] + r); }, &z);
+  };
+  fcn_density_pass(a.w, a.n, dens);
+}
+
+int validate_density(const hk_density_t* m) {
+  HK_REQUIRE(m != nullptr, "NULL model");
+  HK_REQUIRE(m->n_obs >= 1 && m->n_obs <= HK_FCN_MAX_OBS, "observable count %d outside 1..%d",
+             m->n_obs, HK_FCN_MAX_OBS);
+  HK_REQUIRE(m->n_comp >= 1 && m->n_comp <= HK_MAX_COMPONENTS, "component count %d outside 1..%d",
+             m->n_comp, HK_MAX_COMPONENTS);
+  if (int rc = validate_program(&m->program, m->n_obs)) return rc;
+  for (int k = 0; k < m->n_comp; ++k)
+    HK_REQUIRE(m->pdf_slot[k] >= 0 && m->pdf_slot[k] < HK_MAX_SLOTS, "pdf slot %d", m->pdf_slot[k]);
+  return HK_OK;
+}
+
+struct RatioArgs {
+  const double* cols[HK_FCN_MAX_OBS];
+  int64_t n;
+  hk_density_t m;
+  double* part;
+  unsigned long long* bad;  // [0] d not > 0, [1] d not > 0 or non-finite, [2] zero divisor
+  const double* V;          // sPlot: K x K (device copy in the args below)
+};
+
+// per event: p_k (pinned program slots) and d = sum_k N_k p_k (p @ N,
+// fitting.py:416 / splot.py:37); flags as documented in the header
+template <int K>
+__device__ __forceinline__ double ratio_event(const RatioArgs& a, int64_t r, double (&p)[K]) {
+  double slots[HK_MAX_SLOTS];
+  bool z = false;
+  run_program_into(a.m.program, [&](int c) { return __ldg(a.cols[c] + r); }, &z, slots);
+  double d = 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    p[k] = slots[a.m.pdf_slot[k]];
+    d = k == 0 ? p[k] * a.m.yield[k] : d + p[k] * a.m.yield[k];
+  }
+  if (z) record_bad(a.bad + 2, (uint64_t)r);
+  if (!(d > 0.0)) record_bad(a.bad, (uint64_t)r);
+  if (!(d > 0.0) || !isfinite(d)) record_bad(a.bad + 1, (uint64_t)r);
+  return d;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_ratio_program(const __grid_constant__ RatioArgs a) {
+  constexpr int W = K + K * K;
+  const int64_t chunks = (a.n + HK_CHUNK - 1) / HK_CHUNK;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    double acc[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc[w] = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < kRowsPerThread; ++i) {
+      const int64_t r = ch * HK_CHUNK + i * kBlock + threadIdx.x;
+      if (r >= a.n) continue;
+      double p[K];
+      const double d = ratio_event<K>(a, r, p);
+#pragma unroll
+      for (int k = 0; k < K; ++k) p[k] = p[k] / d;  // ratios = p / dens (fitting.py:421)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        acc[k] += p[k];
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[K + k * K + j] += p[k] * p[j];
+      }
+    }
+    block_sum_store<W>(acc, a.part + (int64_t)W * ch);
+  }
+}
+
+struct SplotProgArgs {
+  RatioArgs r;
+  double V[HK_MAX_COMPONENTS * HK_MAX_COMPONENTS];
+  double* out[HK_MAX_COMPONENTS];
+};
+
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_splot_program(const __grid_constant__ SplotProgArgs a) {
+  const int64_t r = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+  if (r >= a.r.n) return;
+  double p[K];
+  const double d = ratio_event<K>(a.r, r, p);
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    double num = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) num = j == 0 ? p[j] * a.V[s * K + j] : num + p[j] * a.V[s * K + j];
+    a.out[s][r] = num / d;  // (p @ V.T) / dens (splot.py:114)
+  }
+}
+
+template <template <int> class Kern, class Args>
+int launch_by_k(int K, unsigned grid, cudaStream_t st, const Args& a, const char* what);
+
+#define HK_K_CASES(KERN)                                       \
+  switch (K) {                                                 \
+    case 1: KERN<1><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 2: KERN<2><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 3: KERN<3><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 4: KERN<4><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 5: KERN<5><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 6: KERN<6><<<grid, kBlock, 0, st>>>(a); break;        \
+    case 7: KERN<7><<<grid, kBlock, 0, st>>>(a); break;        \
+    default: KERN<8><<<grid, kBlock, 0, st>>>(a); break;       \
+  }
+
+int fill_ratio_args(const double* const* d_obs, int64_t n, const hk_density_t* m, RatioArgs* a) {
+  if (int rc = validate_density(m)) return rc;
+  HK_REQUIRE(n >= 0, "negative n");
+  HK_REQUIRE(n == 0 || d_obs, "NULL observables");
+  std::memset(a, 0, sizeof(*a));
+  for (int c = 0; c < m->n_obs && n > 0; ++c) {
+    HK_REQUIRE(d_obs[c], "observable column %d NULL", c);
+    a->cols[c] = d_obs[c];
+  }
+  a->n = n;
+  a->m = *m;
+  return HK_OK;
+}
+
 }  // namespace hk
 
 using namespace hk;
@@ -551,10 +647,92 @@ using namespace hk;
 extern "C" {
 
 int64_t hk_nll_work_doubles(int64_t n) {
-  if (n <= 0) return 4;
+  if (n <= 0) return kFcnWorkHead;
   int64_t full, tail;
   fcn_schedule(n, &full, &tail);
-  return 4 + full + tail;
+  return kFcnWorkHead + full + tail;
+}
+
+int hk_nll_program_eval(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                        double* d_work, double* h_logsum, uint64_t* h_first_bad,
+                        uint64_t* h_first_div0, void* stream) {
+  if (int rc = validate_density(model)) return rc;
+  HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
+  HK_REQUIRE(d_obs && d_work && (!h_logsum || h_first_bad), "NULL pointer");
+  FcnProgArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < model->n_obs; ++c) {
+    HK_REQUIRE(d_obs[c], "observable column %d NULL", c);
+    a.cols[c] = d_obs[c];
+  }
+  a.n = n;
+  a.prog = model->program;
+  Mailbox* mb = nullptr;
+  if (int rc = fcn_setup(d_work, n, &a.w, h_logsum ? &mb : nullptr)) return rc;
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = chunk_grid(a.w.full + a.w.tail_ctas);
+  const void* jit = nullptr;
+  if (int rc = jit_fcn(model->program, n, &jit)) return rc;
+  if (jit) {
+    void* args[] = {&a};
+    HK_CUDA(cudaLaunchKernel(jit, dim3(grid), dim3(kBlock), args, 0, st));
+  } else {
+    k_nll_program<<<grid, kBlock, 0, st>>>(a);
+    if (int rc = check_launch("k_nll_program")) return rc;
+  }
+  if (!h_logsum) return HK_OK;
+  return fcn_wait(mb, a.w.seq, st, "hk_nll_program_eval", h_logsum, h_first_bad, h_first_div0);
+}
+
+int hk_nll_combine(const double* d_gathered, int32_t world, double* h_logsum, uint64_t* h_first_bad,
+                   uint64_t* h_first_div0, void* stream) {
+  HK_REQUIRE(world >= 1 && d_gathered && h_logsum && h_first_bad, "bad combine arguments");
+  Mailbox* mb = nullptr;
+  if (int rc = mailbox(&mb)) return rc;
+  FcnWork w;
+  std::memset(&w, 0, sizeof(w));
+  w.host_mail = mb->d;
+  w.seq = ++mb->seq;
+  cudaStream_t st = as_stream(stream);
+  k_nll_combine<<<1, 32, 0, st>>>(d_gathered, world, w);
+  if (int rc = check_launch("k_nll_combine")) return rc;
+  return fcn_wait(mb, w.seq, st, "hk_nll_combine", h_logsum, h_first_bad, h_first_div0);
+}
+
+int hk_ratio_partials_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                              double* d_partials, uint64_t* d_first_bad, void* stream) {
+  RatioArgs a;
+  if (int rc = fill_ratio_args(d_obs, n, model, &a)) return rc;
+  if (n == 0) return HK_OK;
+  HK_REQUIRE(d_partials && d_first_bad, "NULL pointer");
+  a.part = d_partials;
+  a.bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  const int K = model->n_comp;
+  const unsigned grid = chunk_grid(num_chunks(n));
+  cudaStream_t st = as_stream(stream);
+  HK_K_CASES(k_ratio_program)
+  return check_launch("k_ratio_program");
+}
+
+int hk_splot_weights_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
+                             const double* V, double* const* d_out, uint64_t* d_first_bad,
+                             void* stream) {
+  SplotProgArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (int rc = fill_ratio_args(d_obs, n, model, &a.r)) return rc;
+  const int K = model->n_comp;
+  HK_REQUIRE(V && d_out && d_first_bad, "NULL pointer");
+  for (int i = 0; i < K * K; ++i) a.V[i] = V[i];
+  for (int s = 0; s < K; ++s) {
+    HK_REQUIRE(d_out[s] || n == 0, "output column %d NULL", s);
+    a.out[s] = d_out[s];
+  }
+  if (n == 0) return HK_OK;
+  a.r.bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  const unsigned grid = (unsigned)((n + kBlock - 1) / kBlock);
+  cudaStream_t st = as_stream(stream);
+  HK_K_CASES(k_splot_program)
+  return check_launch("k_splot_program");
 }
 
 int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
@@ -573,20 +751,12 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   Coeffs c;
   if (int rc = make_coeffs(model, &c)) return rc;
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
-  HK_REQUIRE(d_x && d_work && h_logsum && h_first_bad, "NULL pointer");
+  HK_REQUIRE(d_x && d_work && (!h_logsum || h_first_bad), "NULL pointer");
   cudaStream_t st = as_stream(stream);
-  // d_work layout (zero-filled once by the caller, re-armed by the kernel):
-  // [0] sum of logs, [1] first bad row, [2] ~bad-row cell, [3] CTA ticket, [4..] partials
   FcnWork w;
-  w.out = d_work;
-  w.bad = reinterpret_cast<unsigned long long*>(d_work + 2);
-  w.ticket = reinterpret_cast<unsigned int*>(d_work + 3);
-  w.part = d_work + 4;
   Mailbox* mb = nullptr;
-  if (int rc = mailbox(&mb)) return rc;
-  w.host_mail = mb->d;
-  w.seq = ++mb->seq;
-  fcn_schedule(n, &w.full, &w.tail_ctas);
+  if (int rc = fcn_setup(d_work, n, &w, h_logsum ? &mb : nullptr)) return rc;
+  w.div0 = nullptr;  // the closed-form shapes have no divisions to check
   const unsigned grid = chunk_grid(w.full + w.tail_ctas);
   switch (fcn_variant(c)) {
     case kFcnFactored: k_nll_fused<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
@@ -594,25 +764,8 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
     default: k_nll_fused<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
   }
   if (int rc = check_launch("k_nll_fused")) return rc;
-  // The last CTA writes the result into mapped host memory and then the
-  // sequence number; spin on it (no memcpy, no stream sync on the fast path).
-  // Every 4096 polls the stream is queried so a faulted kernel cannot hang us.
-  for (unsigned spins = 1;; ++spins) {
-    if (mb->h[0] == w.seq) break;
-    if ((spins & 4095u) == 0) {
-      const cudaError_t q = cudaStreamQuery(st);
-      if (q == cudaSuccess) {
-        if (mb->h[0] == w.seq) break;
-        set_error("hk_nll_eval: kernel finished without publishing its result");
-        return HK_ECUDA;
-      }
-      if (q != cudaErrorNotReady) return cuda_fail(q, "hk_nll_eval");
-    }
-  }
-  const unsigned long long sum_bits = mb->h[1];
-  std::memcpy(h_logsum, &sum_bits, sizeof(double));
-  *h_first_bad = mb->h[2];
-  return HK_OK;
+  if (!h_logsum) return HK_OK;
+  return fcn_wait(mb, w.seq, st, "hk_nll_eval", h_logsum, h_first_bad, nullptr);
 }
 
 int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,

@@ -50,6 +50,13 @@ struct JitArgs {
 int jit_kernel(const hk_program_t& P, int64_t rows, int kind, const void** fn);
 // same for the fused generate+integrate kernel (n daughters, RNG mode)
 int jit_integrate(const hk_program_t& P, int n, int mode, int64_t rows, const void** fn);
+// the program-driven FCN pass (hk_fcn.cuh fcn_density_pass) with the density
+// program inlined; constants are read from the kernel's FcnProgArgs, so one
+// module serves every parameter point of a model structure
+int jit_fcn(const hk_program_t& P, int64_t rows, const void** fn);
+
+// hk_phsp.cu: structural check of a program reading n_cols columns
+int validate_program(const hk_program_t* f, int n_cols);
 
 }  // namespace hk
 

@@ -92,7 +92,9 @@ std::string hex_const(double v) {
 // that last wrote them (the program is in execution order).  Column c reads
 // HBM (stored block) or the register-resident event (fused: c = 0 is the
 // weight w, c = 1 + 4 j + k is p[4 j + k]).  Zero divisors set d0.
-std::string emit_body(const hk_program_t& P, bool fused) {
+// params: constants come from the kernel arguments (a.prog.cst[i]) instead of
+// being baked in -- the FCN module, compiled once per op structure.
+std::string emit_body(const hk_program_t& P, bool fused, bool params = false) {
   std::string s;
   int slot_of[HK_MAX_SLOTS];
   for (int& x : slot_of) x = -1;
@@ -103,7 +105,8 @@ std::string emit_body(const hk_program_t& P, bool fused) {
     const bool leaf = P.op[i] == HK_OP_COL || P.op[i] == HK_OP_CONST;
     const std::string A = leaf ? "" : v(P.a[i]);
     const std::string B = leaf ? "" : v(P.b[i]);
-    const std::string c1 = hex_const(P.cst[i]), c2 = hex_const(P.cst2[i]);
+    const std::string c1 = params ? "a.prog.cst[" + std::to_string(i) + "]" : hex_const(P.cst[i]);
+    const std::string c2 = params ? "a.prog.cst2[" + std::to_string(i) + "]" : hex_const(P.cst2[i]);
     std::string e;
     switch (P.op[i]) {
       case HK_OP_COL:
@@ -137,6 +140,7 @@ std::string emit_body(const hk_program_t& P, bool fused) {
         break;
       case HK_OP_ADD0: e = "__dadd_rn(" + A + ", 0.0)"; break;
       case HK_OP_SQUARE: e = "__dmul_rn(" + A + ", " + A + ")"; break;
+      case HK_OP_UDIV: e = "__ddiv_rn(" + A + ", " + B + ")"; break;
       default: e = "__longlong_as_double(0x7ff8000000000000ll)"; break;
     }
     s += "  const double v" + std::to_string(i) + " = " + e + ";\n";
@@ -249,8 +253,36 @@ const EmbeddedHeader kHeaders[] = {
 };
 constexpr int kNumHeaders = sizeof(kHeaders) / sizeof(kHeaders[0]);
 
-// n == 0: stored-block module; else fused generate+integrate for n daughters
+// n == -1: the FCN module (hk_fcn.cuh fcn_density_pass with the density
+// program inlined, constants from the arguments)
+const char* kFcnPrelude = R"(
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long int64_t;
+typedef unsigned long uint64_t;
+typedef unsigned long size_t;
+#define UINT64_MAX 0xffffffffffffffffUL
+#include "hk_fcn.cuh"
+)";
+
+// n == 0: stored-block module; n > 0: fused generate+integrate for n daughters
 std::string full_source(const hk_program_t& P, int n, int mode) {
+  if (n < 0)
+    return std::string(kFcnPrelude) +
+           "struct HkDensity {\n"
+           "  const hk::FcnProgArgs& a;\n"
+           "  __device__ __forceinline__ double operator()(long long r, bool& d0) const {\n" +
+           emit_body(P, false, true) +
+           "  }\n"
+           "};\n"
+           "extern \"C\" __global__ void __launch_bounds__(256)\n"
+           "    hk_jit_nll(const __grid_constant__ hk::FcnProgArgs a) {\n"
+           "  hk::fcn_density_pass(a.w, a.n, HkDensity{a});\n"
+           "}\n";
   if (n == 0)
     return "#define HK_JIT_MAX_COLS " + std::to_string(kJitMaxCols) + "\n" + kStoredPrelude +
            "__device__ __forceinline__ double hk_f(const JitArgs& a, long long r, bool& d0) {\n" +
@@ -309,8 +341,10 @@ std::string cache_key(const hk_program_t& P, int n, int mode) {
     put(&P.dst[i], 4);
     put(&P.a[i], 4);
     put(&P.b[i], 4);
-    put(&P.cst[i], 8);
-    put(&P.cst2[i], 8);
+    if (n >= 0) {  // the FCN module (n = -1) reads its constants at run time
+      put(&P.cst[i], 8);
+      put(&P.cst2[i], 8);
+    }
   }
   return k;
 }
@@ -360,7 +394,9 @@ int compile_entry(const hk_program_t& P, int n, int mode, Entry* out) {
   std::vector<char> cubin;
   if (int rc = compile_cubin(P, n, mode, &cubin)) return rc;
   HK_CUDA(cudaLibraryLoadData(&out->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-  if (n == 0) {
+  if (n < 0) {
+    HK_CUDA(cudaLibraryGetKernel(&out->kern[0], out->lib, "hk_jit_nll"));
+  } else if (n == 0) {
     HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMoments], out->lib, "hk_jit_moments"));
     HK_CUDA(cudaLibraryGetKernel(&out->kern[kJitMap], out->lib, "hk_jit_map"));
   } else {
@@ -400,6 +436,10 @@ int jit_integrate(const hk_program_t& P, int n, int mode, int64_t rows, const vo
   return lookup(P, n, mode, rows, 0, fn);
 }
 
+int jit_fcn(const hk_program_t& P, int64_t rows, const void** fn) {
+  return lookup(P, -1, 0, rows, 0, fn);
+}
+
 // hk_shutdown: unload every specialised module (no launch may be in flight)
 void jit_release() {
   std::lock_guard<std::mutex> lock(g_mu);
@@ -427,7 +467,7 @@ int hk_set_jit_mode(int32_t mode) {
 
 int64_t hk_jit_source(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, char* buf,
                       int64_t cap) {
-  if (!f || f->n_ops < 1 || f->n_ops > HK_MAX_PROGRAM || n_daughters < 0 || n_daughters > 8 ||
+  if (!f || f->n_ops < 1 || f->n_ops > HK_MAX_PROGRAM || n_daughters < -1 || n_daughters > 8 ||
       n_daughters == 1 || rng_mode < 0 || rng_mode > 1) {
     set_error("bad program / target");
     return -1;
@@ -443,7 +483,8 @@ int64_t hk_jit_source(const hk_program_t* f, int32_t n_daughters, int32_t rng_mo
 
 int hk_jit_compile(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, int64_t* cubin_bytes) {
   HK_REQUIRE(f && f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "bad program");
-  HK_REQUIRE(n_daughters == 0 || (n_daughters >= 2 && n_daughters <= 8), "n_daughters %d", n_daughters);
+  HK_REQUIRE(n_daughters == -1 || n_daughters == 0 || (n_daughters >= 2 && n_daughters <= 8),
+             "n_daughters %d", n_daughters);
   HK_REQUIRE(rng_mode == HK_RNG_REFERENCE || rng_mode == HK_RNG_PHILOX, "rng mode %d", rng_mode);
   std::vector<char> cubin;
   {

@@ -596,11 +596,13 @@ __global__ void k_philox_rows(const uint32_t* in6, int64_t n, uint32_t* out4) {
 // same n_parts -> same bits, whatever produced them.
 constexpr int kFoldCtas = 8;  // portable cluster size
 constexpr int kFoldThreads = 1024;
+// widest record folded: the ratio sums of HK_MAX_COMPONENTS species, K + K^2
+constexpr int kFoldMaxWidth = HK_MAX_COMPONENTS + HK_MAX_COMPONENTS * HK_MAX_COMPONENTS;
 
 __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads)
     k_fold(const double* parts, int64_t n, int width, double* out) {
-  __shared__ double sm[32][32];  // [warp][w]
-  __shared__ double cta_sum[32];
+  __shared__ double sm[32][kFoldMaxWidth];  // [warp][w]
+  __shared__ double cta_sum[kFoldMaxWidth];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -812,7 +814,7 @@ int validate_program(const hk_program_t* f, int n_cols) {
   HK_REQUIRE(f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "program length %d", f->n_ops);
   HK_REQUIRE(f->result >= 0 && f->result < HK_MAX_SLOTS, "program result slot %d", f->result);
   for (int i = 0; i < f->n_ops; ++i) {
-    HK_REQUIRE(f->op[i] >= HK_OP_COL && f->op[i] <= HK_OP_SQUARE, "op %d: bad opcode %d", i,
+    HK_REQUIRE(f->op[i] >= HK_OP_COL && f->op[i] <= HK_OP_UDIV, "op %d: bad opcode %d", i,
                f->op[i]);
     HK_REQUIRE(f->dst[i] >= 0 && f->dst[i] < HK_MAX_SLOTS, "op %d: bad dst", i);
     if (f->op[i] == HK_OP_COL) {
@@ -1085,7 +1087,7 @@ int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_l
 int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chunk_begin,
                    int64_t n_chunks_local, int32_t recs_per_chunk, int32_t width, int32_t s_begin,
                    int32_t s_count, double* d_out, void* stream) {
-  HK_REQUIRE(width >= 1 && width <= 32 && recs_per_chunk >= 1 && recs_per_chunk <= 1024,
+  HK_REQUIRE(width >= 1 && width <= kFoldMaxWidth && recs_per_chunk >= 1 && recs_per_chunk <= 1024,
              "bad record shape %d x %d", recs_per_chunk, width);
   HK_REQUIRE(n_chunks_total >= 0 && chunk_begin >= 0 && n_chunks_local >= 0 &&
                  chunk_begin + n_chunks_local <= n_chunks_total,
@@ -1111,7 +1113,7 @@ int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chu
 
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,
                      void* stream) {
-  HK_REQUIRE(width >= 1 && width <= 32, "fold width %d outside 1..32", width);
+  HK_REQUIRE(width >= 1 && width <= kFoldMaxWidth, "fold width %d outside 1..%d", width, kFoldMaxWidth);
   HK_REQUIRE(n_parts >= 0 && d_out, "bad fold arguments");
   HK_REQUIRE(n_parts == 0 || d_partials, "NULL partials");
   return launch_fold(d_partials, n_parts, width, d_out, as_stream(stream));

@@ -81,7 +81,7 @@ class ParamSet:
 # symbolic tracing: a DAG of hash-consed tuples
 #   ("col", c) ("const", v) (op, a, b) (unary, a) ("gauss", a, mu, s) ...
 
-_BINARY = {"add", "sub", "mul", "div"}
+_BINARY = {"add", "sub", "mul", "div", "udiv"}
 _UNARY = {"neg", "sqrt", "exp", "log", "square", "add0"}
 
 
@@ -114,8 +114,10 @@ class Sym:
     def __rsub__(self, o): return self._bin("sub", o, True)
     def __mul__(self, o): return self._bin("mul", o)
     def __rmul__(self, o): return self._bin("mul", o, True)
-    def __truediv__(self, o): return self._bin("div", o)
-    def __rtruediv__(self, o): return self._bin("div", o, True)
+    # numpy division in traced code never raises (inf / nan, as in the
+    # reference's closures and arg_builders): unchecked "udiv"
+    def __truediv__(self, o): return self._bin("udiv", o)
+    def __rtruediv__(self, o): return self._bin("udiv", o, True)
     def __neg__(self): return Sym(("neg", self.node))
     def __pos__(self): return self
 
@@ -132,8 +134,8 @@ class Sym:
     def __bool__(self):
         raise NotImplementedError("data-dependent control flow cannot be lowered to the device")
 
-    _UFUNCS = {"add": "add", "subtract": "sub", "multiply": "mul", "divide": "div",
-               "true_divide": "div", "negative": "neg", "sqrt": "sqrt", "exp": "exp",
+    _UFUNCS = {"add": "add", "subtract": "sub", "multiply": "mul", "divide": "udiv",
+               "true_divide": "udiv", "negative": "neg", "sqrt": "sqrt", "exp": "exp",
                "log": "log", "square": "square", "power": "power", "positive": None}
 
     def __array_ufunc__(self, ufunc, method, *inputs, **kwargs):
@@ -461,7 +463,7 @@ def identity() -> FunctorExpr:
 
 _OPCODE = {"add": _lib.OP_ADD, "sub": _lib.OP_SUB, "mul": _lib.OP_MUL, "div": _lib.OP_DIV,
            "neg": _lib.OP_NEG, "sqrt": _lib.OP_SQRT, "exp": _lib.OP_EXP, "log": _lib.OP_LOG,
-           "square": _lib.OP_SQUARE, "add0": _lib.OP_ADD0}
+           "square": _lib.OP_SQUARE, "add0": _lib.OP_ADD0, "udiv": _lib.OP_UDIV}
 
 
 def _children(node) -> list:
@@ -477,12 +479,17 @@ def _is_leaf(node) -> bool:
     return node[0] in ("col", "const")
 
 
-def compile_program(root) -> "_lib.hk_program_t":
+def compile_program(root, keep: Sequence = (), params: Sequence[float] | None = None):
     """Hash-consed DAG -> SSA ops in dependency order with liveness-based slots.
 
     Interior nodes are computed once (common subexpressions shared); leaves
     (column loads, constants) are re-issued right before each use so they
-    never hold a register across the program.
+    never hold a register across the program.  ``keep`` lists further nodes
+    whose values must survive to the end (multi-output programs, e.g. the
+    per-component p.d.f.s next to the density); with ``keep`` the result is
+    (program, slot of each kept node).  A constant ("const", ("p", k)) is the
+    k-th of ``params`` (parametric programs: the structure is fixed, the
+    values change per call -- see lower_density).
     """
     order: list = []                 # node per op
     args_of: list = []               # operand op indices per op
@@ -493,7 +500,8 @@ def compile_program(root) -> "_lib.hk_program_t":
         args_of.append(operands)
         return len(order) - 1
 
-    stack = [(root, False)]
+    roots = [root, *keep]
+    stack = [(r, False) for r in reversed(roots)]
     while stack:                     # iterative post-order over interior nodes
         node, done = stack.pop()
         if _is_leaf(node):
@@ -510,7 +518,8 @@ def compile_program(root) -> "_lib.hk_program_t":
         stack.append((node, True))
         for ch in reversed(_children(node)):
             stack.append((ch, False))
-    root_op = emit(root, []) if _is_leaf(root) else index[root]
+    root_ops = [emit(r, []) if _is_leaf(r) else index[r] for r in roots]
+    pinned = set(root_ops)
     if len(order) > _lib.HK_MAX_PROGRAM:
         raise NotImplementedError(f"expression needs {len(order)} device ops "
                                   f"(limit {_lib.HK_MAX_PROGRAM})")
@@ -525,7 +534,7 @@ def compile_program(root) -> "_lib.hk_program_t":
     for i, node in enumerate(order):
         src = [slot[j] for j in args_of[i]]
         for j in set(args_of[i]):    # operands whose last use is here free their slot
-            if last_use.get(j) == i and j != root_op:
+            if last_use.get(j) == i and j not in pinned:
                 free.append(slot[j])
         if not free:
             raise NotImplementedError("expression needs more than "
@@ -541,7 +550,8 @@ def compile_program(root) -> "_lib.hk_program_t":
             prog.a[i] = node[1]
         elif kind == "const":
             prog.op[i] = _lib.OP_CONST
-            prog.cst[i] = node[1]
+            v = node[1]
+            prog.cst[i] = params[v[1]] if isinstance(v, tuple) else v
         elif kind == "gauss":
             prog.op[i], prog.cst[i], prog.cst2[i] = _lib.OP_GAUSS, node[2], node[3]
         elif kind == "expo":
@@ -550,8 +560,69 @@ def compile_program(root) -> "_lib.hk_program_t":
             prog.op[i], prog.cst[i], prog.cst2[i] = _lib.OP_BW, node[2], node[3]
         else:
             prog.op[i] = _OPCODE[kind]
-    prog.result = slot[root_op]
+    prog.result = slot[root_ops[0]]
+    if keep:
+        return prog, [slot[r] for r in root_ops[1:]]
     return prog
+
+
+def desugar(node):
+    """Builtin shape ops (gauss/expo/bw, which carry their parameters inside
+    the op) rewritten as primitive ops with constant leaves, in the
+    reference's operation order (functors.py:142-143, :161), so that a
+    parametric program can vary those parameters per call."""
+    memo: dict = {}
+
+    def walk(n):
+        key = id(n)
+        if key in memo:
+            return memo[key]
+        kind = n[0]
+        if kind in ("col", "const"):
+            out = n
+        elif kind == "gauss":
+            a, mu, s = walk(n[1]), ("const", n[2]), ("const", n[3])
+            z = ("udiv", ("sub", a, mu), s)
+            out = ("udiv", ("exp", ("mul", ("mul", ("const", -0.5), z), z)), ("mul", s, ("const", _SQRT_2PI)))
+        elif kind == "expo":
+            out = ("exp", ("udiv", ("neg", walk(n[1])), ("const", n[2])))
+        elif kind == "bw":
+            m0, g0 = ("const", n[2]), ("const", n[3])
+            m2 = ("mul", m0, m0)
+            t = ("sub", walk(n[1]), m2)
+            out = ("udiv", ("const", 1.0), ("add", ("mul", t, t), ("mul", m2, ("mul", g0, g0))))
+        else:
+            out = (kind, *[walk(c) for c in n[1:]])
+        memo[key] = out
+        return out
+
+    return walk(node)
+
+
+def parametrize(roots: Sequence) -> tuple[tuple, list[float]]:
+    """Lift every constant of a (desugared) IR DAG into a parameter slot:
+    returns (roots with ("const", ("p", k)) leaves, [value_k]).  Shared
+    sub-DAGs (same object) stay shared; the structure no longer depends on
+    the values, so one compiled program serves every parameter point."""
+    memo: dict = {}
+    values: list[float] = []
+
+    def walk(n):
+        key = id(n)
+        if key in memo:
+            return memo[key]
+        kind = n[0]
+        if kind == "const":
+            out = ("const", ("p", len(values)))
+            values.append(float(n[1]))
+        elif kind == "col":
+            out = n
+        else:
+            out = (kind, *[walk(c) for c in n[1:]])
+        memo[key] = out
+        return out
+
+    return tuple(walk(r) for r in roots), values
 
 
 def lower_average(expr: FunctorExpr, arg_builder, names: Sequence[str], with_root: bool = False):
@@ -612,7 +683,7 @@ def eval_node(node, cols: dict[int, float]) -> float:
             return x - v[1]
         if kind == "mul":
             return x * v[1]
-        if kind == "div":
+        if kind in ("div", "udiv"):
             return x / v[1]
         if kind == "neg":
             return -x

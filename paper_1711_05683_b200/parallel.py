@@ -187,44 +187,104 @@ def shard_rows(store, rank: int, world: int):
     return ColumnStore._from_device(store.schema, cols), a
 
 
+_PART = 3 + _lib.HK_FCN_MAX_OBS   # host-path record: logsum, global row (-1), kind, payload
+
+
 def combine_nll_parts(parts, expected_total: float) -> float:
-    """Fold per-rank (event log-sum, global first-bad row or -1, its density)
-    triples in rank order: deterministic for a fixed GPU count.  The smallest
-    bad row wins, as in the reference (fitting.py:200-205)."""
-    import numpy as np  # noqa: PLC0415
-    bad = [(int(row), val) for _, row, val in parts if row >= 0]
-    if bad:
-        row, val = min(bad)
-        raise ValueError(f"model density {np.float64(val)!r} is not positive at event {row}")
+    """Fold per-rank records (event log-sum, global problem row or -1, kind,
+    payload...) in rank order: deterministic for a fixed GPU count.  The
+    problem the reference would raise wins (fitting.first_problem: earliest
+    batch, zero divisor before density, smallest row)."""
+    from .fitting import DIV0, EVAL_BATCH_ROWS, fcn_exception  # noqa: PLC0415
+    probs = [(int(p[1]) // EVAL_BATCH_ROWS, int(p[2]), int(p[1]), p) for p in parts if p[1] >= 0]
+    if probs:
+        _, kind, row, p = min(probs, key=lambda t: t[:3])
+        if kind == DIV0:
+            payload = tuple(np.float64(v) for v in p[3:3 + int(p[-1])])
+        else:
+            payload = np.float64(p[3])
+        raise fcn_exception(row, kind, payload)
     total = 0.0
-    for logsum, _, _ in parts:
-        total += logsum
+    for p in parts:
+        total += p[0]
     return expected_total - total
 
 
-def sharded_nll(model, shard, observable_columns, row_offset: int, group=None) -> float:
+def sharded_nll(model, shard, observable_columns, row_offset: int, group=None,
+                _force_collective: bool = False) -> float:
     """nll (fitting.py:175-210) over a data set split by row range across the
-    process group: each rank runs the fused FCN pass over its resident rows,
-    then one all-gather of 3 doubles per rank and the same rank-order fold on
-    every rank, so all ranks return the same value (a minimiser can run in
+    process group; every rank returns the same value (a minimiser can run in
     lock-step on every rank).  `row_offset` is the shard's first global row,
-    so a bad event is reported by its global index."""
-    from .fitting import nll_event_sum  # noqa: PLC0415
+    so a bad event is reported by its global index.
+
+    Over NCCL one evaluation is: the fused FCN pass enqueued without waiting
+    (fitting.nll_event_launch), one stream-ordered all-gather of each rank's
+    8-double record, and hk_nll_combine -- a kernel that folds the records in
+    rank order and publishes the result into mapped host memory -- so the
+    host synchronises once.  Other backends (gloo: the CPU tests of this
+    logic) exchange the same records through host memory."""
+    from . import fitting  # noqa: PLC0415
     rank, world = dist_info(group)
-    if len(shard):
-        logsum, first, val = nll_event_sum(model, shard, observable_columns)
-    else:
-        logsum, first, val = 0.0, None, None
-    if world == 1:
-        if first is not None:
-            raise ValueError(f"model density {val!r} is not positive at event {row_offset + first}")
+    if world == 1 and not _force_collective:   # (forced: test hook for a 1-rank NCCL group)
+        logsum, problem = fitting.nll_event_sum(model, shard, observable_columns) if len(shard) else (0.0, None)
+        if problem is not None:
+            row, kind, payload = problem
+            raise fitting.fcn_exception(row_offset + row, kind, payload)
         return model.expected_total() - logsum
-    mine = (logsum, -1.0 if first is None else float(row_offset + first), 0.0 if val is None else float(val))
     torch = _lib.torch()
     dist = torch.distributed
-    dev = _lib.device() if dist.get_backend(group) == "nccl" else "cpu"
-    t = torch.tensor(mine, dtype=torch.float64, device=dev)
+    if dist.get_backend(group) != "nccl":
+        return _sharded_nll_host(model, shard, observable_columns, row_offset, group)
+    none = np.array([-1], dtype=np.int64).view(np.float64)[0]
+    if len(shard):
+        work = fitting.nll_event_launch(model, shard, observable_columns)
+        work[6] = float(row_offset)
+        rec = work[:8]
+    else:
+        rec = torch.from_numpy(np.array([0.0, none, 0, 0, 0, none, float(row_offset), 0.0])).to(_lib.device())
+    gathered = torch.empty(world * 8, dtype=torch.float64, device=rec.device)
+    dist.all_gather_into_tensor(gathered, rec, group=group)
+    logsum = _lib.ctypes.c_double()
+    bad, zero = _lib.ctypes.c_uint64(), _lib.ctypes.c_uint64()
+    _lib.check(_lib.lib().hk_nll_combine(gathered.data_ptr(), world, _lib.ctypes.byref(logsum),
+                                         _lib.ctypes.byref(bad), _lib.ctypes.byref(zero), _lib.stream_ptr()),
+               "hk_nll_combine")
+    problem = fitting.first_problem(zero.value, bad.value)
+    if problem is None:
+        return model.expected_total() - logsum.value
+    # slow path: the owning rank computes the message payload, everyone raises
+    row, kind = problem
+    mine = np.zeros(2 + _lib.HK_FCN_MAX_OBS)
+    if row_offset <= row < row_offset + len(shard):
+        pay = fitting.problem_payload(model, shard, observable_columns, row - row_offset, kind)
+        vals = list(pay) if kind == fitting.DIV0 else [float(pay)]
+        mine[0], mine[1] = 1.0, len(vals)
+        mine[2:2 + len(vals)] = vals
+    recs = torch.empty(world * mine.size, dtype=torch.float64, device=rec.device)
+    dist.all_gather_into_tensor(recs, torch.from_numpy(mine).to(rec.device), group=group)
+    owner = next(r for r in recs.view(world, -1).cpu().numpy() if r[0] == 1.0)
+    vals = owner[2:2 + int(owner[1])]
+    payload = tuple(np.float64(v) for v in vals) if kind == fitting.DIV0 else np.float64(vals[0])
+    raise fitting.fcn_exception(row, kind, payload)
+
+
+def _sharded_nll_host(model, shard, observable_columns, row_offset: int, group=None) -> float:
+    from . import fitting  # noqa: PLC0415
+    torch = _lib.torch()
+    dist = torch.distributed
+    _, world = dist_info(group)
+    rec = np.zeros(_PART + 1)
+    rec[1] = -1.0
+    if len(shard):
+        logsum, problem = fitting.nll_event_sum(model, shard, observable_columns)
+        rec[0] = logsum
+        if problem is not None:
+            row, kind, payload = problem
+            vals = list(payload) if kind == fitting.DIV0 else [float(payload)]
+            rec[1], rec[2] = float(row_offset + row), float(kind)
+            rec[3:3 + len(vals)] = vals
+            rec[-1] = len(vals)
+    t = torch.from_numpy(rec)
     out = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(out, t, group=group)
-    parts = torch.stack(out).cpu().tolist()
-    return combine_nll_parts([tuple(p) for p in parts], model.expected_total())
+    return combine_nll_parts([o.numpy() for o in out], model.expected_total())

@@ -14,7 +14,8 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from .fitting import ExtendedModel, _observable, lower_model, ratio_sums
+from .fitting import (DENSITY, DIV0, ExtendedModel, _closed_form, _density_at, _observables, fcn_exception,
+                      first_problem, lower_density, lower_model, ratio_sums)
 from .store import ColumnSchema, ColumnStore
 
 _STATIONARITY_TOL = 1e-6   # splot.py:30
@@ -22,20 +23,34 @@ _CONDITION_LIMIT = 1e12    # splot.py:32
 
 
 def _density_error(model: ExtendedModel, store: ColumnStore, observable_columns, row: int):
-    x = _observable(store, observable_columns, model)
-    cell = _lib.empty(1)
-    _lib.check(_lib.lib().hk_model_density(_lib.ptr(x[row:row + 1]), 1, lower_model(model),
-                                           _lib.ptr(cell), _lib.stream_ptr()), "hk_model_density")
-    d = np.float64(float(cell.item()))
+    obs = _observables(store, observable_columns, model)
+    if _closed_form(model):
+        cell = _lib.empty(1)
+        _lib.check(_lib.lib().hk_model_density(_lib.ptr(obs[0][row:row + 1]), 1, lower_model(model),
+                                               _lib.ptr(cell), _lib.stream_ptr()), "hk_model_density")
+        d = np.float64(float(cell.item()))
+    else:
+        d = _density_at(lower_density(model), obs, row)
     return ValueError(f"model density {d!r} is not positive at event {row}")
+
+
+def _raise_first(model, store, observable_columns, div0_row: int, bad_row: int) -> None:
+    problem = first_problem(div0_row, bad_row)
+    if problem is None:
+        return
+    row, kind = problem
+    if kind == DIV0:
+        obs = _observables(store, observable_columns, model)
+        raise fcn_exception(row, DIV0, tuple(np.float64(float(c[row])) for c in obs))
+    assert kind == DENSITY
+    raise _density_error(model, store, observable_columns, row)
 
 
 def splot_matrix(model: ExtendedModel, store: ColumnStore, observable_columns: Sequence[str],
                  workers: int | None = 1) -> np.ndarray:
     """sWeights covariance matrix V (splot.py:45-87)."""
     g, vinv, bad = ratio_sums(model, store, observable_columns)
-    if bad[1] != _lib.HK_NO_BAD_ROW:
-        raise _density_error(model, store, observable_columns, bad[1])
+    _raise_first(model, store, observable_columns, bad[2], bad[1])
     residual = float(np.max(np.abs(g - 1.0)))
     if residual > _STATIONARITY_TOL:
         raise ValueError(f"yields are not at the extended-ML optimum "
@@ -53,19 +68,23 @@ def splot_weights(model: ExtendedModel, store: ColumnStore, observable_columns: 
     V = np.asarray(V, dtype=float)
     if V.shape != (k, k):
         raise ValueError(f"V must be {k}x{k}, got {V.shape}")
-    if k > 4:
-        raise NotImplementedError("device sWeights support up to 4 species")
-    x = _observable(store, observable_columns, model)
+    obs = _observables(store, observable_columns, model)
     n = len(store)
     cols = [_lib.empty(n) for _ in range(k)]
-    bad = _lib.bad_cells(1)
     vflat = np.ascontiguousarray(V.ravel())
-    _lib.check(_lib.lib().hk_splot_weights(_lib.ptr(x), n, lower_model(model),
-                                           vflat.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_double)),
-                                           _lib.ptr_array(cols), _lib.ptr(bad), _lib.stream_ptr()),
-               "hk_splot_weights")
-    (first,) = _lib.read_bad(bad)
-    if first != _lib.HK_NO_BAD_ROW:
-        raise _density_error(model, store, observable_columns, first)
+    vptr = vflat.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_double))
+    if _closed_form(model) and k <= 4:
+        bad = _lib.bad_cells(1)
+        _lib.check(_lib.lib().hk_splot_weights(_lib.ptr(obs[0]), n, lower_model(model), vptr,
+                                               _lib.ptr_array(cols), _lib.ptr(bad), _lib.stream_ptr()),
+                   "hk_splot_weights")
+        flags = [_lib.HK_NO_BAD_ROW, *_lib.read_bad(bad), _lib.HK_NO_BAD_ROW]
+    else:
+        bad = _lib.bad_cells(3)
+        _lib.check(_lib.lib().hk_splot_weights_program(_lib.ptr_array(obs), n, lower_density(model), vptr,
+                                                       _lib.ptr_array(cols), _lib.ptr(bad), _lib.stream_ptr()),
+                   "hk_splot_weights_program")
+        flags = _lib.read_bad(bad)
+    _raise_first(model, store, observable_columns, flags[2], flags[1])
     schema = ColumnSchema.real64(*(f"sw_{name}" for name in model.species()))
     return ColumnStore._from_device(schema, cols)

@@ -76,6 +76,8 @@ def run_program_numpy(prog, cols: list[np.ndarray]) -> tuple[np.ndarray, np.ndar
                 v = 1.0 / (t * t + (m0 * m0) * (g0 * g0))
             elif op == L.OP_ADD0:
                 v = r[a] + 0.0
+            elif op == L.OP_UDIV:
+                v = r[a] / r[b]
             elif op == L.OP_SQUARE:
                 v = r[a] * r[a]
             else:
@@ -119,4 +121,5 @@ def jit_cases(hk):
         ("coordinate", hk.coordinate(1, 2), lambda c: (c["p1_e"], c["p2_px"])),
         ("square_neg", hk.identity(), lambda c: (-(c["p1_px"] ** 2) - c["weight"],)),
         ("constant", hk.constant(2.5), lambda c: (c["p1_e"],)),
+        ("checked_div", hk.combine("/", hk.identity(), hk.constant(3.0)), m12sq_builder),
     ]

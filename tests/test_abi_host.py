@@ -116,13 +116,34 @@ def test_clique_lifetime_validation(hk):
     assert "hk_init" in _lib.last_error()
 
 
-def test_struct_layouts_match_header(hk):
+def test_struct_layouts_match_header(hk, tmp_path):
+    """Every ctypes mirror has the C compiler's size and field offsets for the
+    structs include/hepkit_cuda.h declares."""
+    import shutil
+    import subprocess
     from paper_1711_05683_b200 import _lib
-    # hk_decay_t: 2 ints + 2 doubles + 2*16 doubles + 4 + 1 doubles
-    assert ctypes.sizeof(_lib.hk_decay_t) == 8 + 16 + 8 * 32 + 8 * 5
-    assert ctypes.sizeof(_lib.hk_key_t) == 32
-    assert ctypes.sizeof(_lib.hk_program_t) == 8 + 4 * 4 * 48 + 8 * 2 * 48
-    assert ctypes.sizeof(_lib.hk_model_t) == 8 + 4 * 8 + 8 * 4 * 8
+    cc = shutil.which("gcc")
+    if cc is None:
+        pytest.skip("no host compiler")
+    structs = {"hk_key_t": _lib.hk_key_t, "hk_decay_t": _lib.hk_decay_t, "hk_program_t": _lib.hk_program_t,
+               "hk_model_t": _lib.hk_model_t, "hk_pair_integrand_t": _lib.hk_pair_integrand_t,
+               "hk_density_t": _lib.hk_density_t}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hepkit_cuda.h"', "int main(void) {"]
+    want = []
+    for cname, py in structs.items():
+        lines.append(f'printf("%zu\\n", sizeof({cname}));')
+        want.append(ctypes.sizeof(py))
+        for fname, _ in py._fields_:
+            cfield = "yield" if fname == "yield_" else fname
+            lines.append(f'printf("%zu\\n", offsetof({cname}, {cfield}));')
+            want.append(getattr(py, fname).offset)
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == want
 
 
 def test_no_device_fails_loudly(hk):

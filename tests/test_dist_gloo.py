@@ -77,12 +77,18 @@ class _Model:
 
 def _fake_event_sum(model, shard, cols):
     """Host stand-in for the GPU pass (fitting.nll_event_sum): sum of logs
-    and the first non-positive row of the shard."""
+    and the first problem of the shard -- a non-positive density, or (for
+    inf entries, standing in for a zero divisor inside a shape) a DIV0."""
+    from paper_1711_05683_b200.fitting import DENSITY, DIV0, first_problem
     d = shard.x
-    bad = np.flatnonzero(~(d > 0))
-    if bad.size:
-        return 0.0, int(bad[0]), np.float64(d[bad[0]])
-    return float(np.sum(np.log(d))), None, None
+    bad = np.flatnonzero(~(d > 0) | np.isnan(d))
+    zero = np.flatnonzero(np.isinf(d))
+    first = first_problem(int(zero[0]) if zero.size else -1, int(bad[0]) if bad.size else -1)
+    if first is None:
+        return float(np.sum(np.log(d))), None
+    row, kind = first
+    payload = (np.float64(d[row]), np.float64(2.0)) if kind == DIV0 else np.float64(d[row])
+    return 0.0, (row, kind, payload)
 
 
 def _nll_worker(rank: int, world: int, port: int, dens: np.ndarray, out_dir: str) -> None:
@@ -102,7 +108,7 @@ def _nll_worker(rank: int, world: int, port: int, dens: np.ndarray, out_dir: str
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["clean", "bad"])
+@pytest.mark.parametrize("case", ["clean", "bad", "div0", "div0_later_batch"])
 def test_sharded_nll_combine(tmp_path, case):
     """Row-sharded FCN (parallel.sharded_nll): every rank returns the same
     value, the rank-order sum of the shard log-sums, and a bad density is
@@ -113,17 +119,25 @@ def test_sharded_nll_combine(tmp_path, case):
     dens = rs.uniform(0.1, 2.0, 3 * 4096 + 17)
     if case == "bad":
         dens[[9000, 8200, 100]] = [0.0, np.nan, -1.0]   # rank 1 holds 8200/9000, rank 0 holds 100
+    if case == "div0":
+        dens[[9000, 100]] = [np.inf, -1.0]   # same 65536-row batch: the zero divisor (rank 1) wins
+    if case == "div0_later_batch":
+        dens = np.concatenate([dens, rs.uniform(0.1, 2.0, 70_000)])
+        dens[[70_000, 100]] = [np.inf, -1.0]  # the density problem's batch comes first
     port = _free_port()
     mp.start_processes(_nll_worker, args=(world, port, dens, str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
     got = [tuple(np.load(tmp_path / f"nll{r}.npy", allow_pickle=True)) for r in range(world)]
     assert got[0] == got[1]
-    if case == "bad":
+    if case in ("bad", "div0_later_batch"):
         assert got[0] == ("err", "model density np.float64(-1.0) is not positive at event 100")
+        return
+    if case == "div0":
+        assert got[0] == ("err", "division by zero at point (np.float64(inf), np.float64(2.0))")
         return
     parts = []
     for r in range(world):
         a, b = shard_range(len(dens), r, world)
-        parts.append((float(np.sum(np.log(dens[a:b]))), -1.0, 0.0))
+        parts.append(np.array([float(np.sum(np.log(dens[a:b]))), -1.0] + [0.0] * 10))
     assert got[0] == ("ok", combine_nll_parts(parts, 123.5))
     assert got[0][1] == pytest.approx(123.5 - float(np.sum(np.log(dens))), rel=1e-12)

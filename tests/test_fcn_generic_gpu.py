@@ -1,0 +1,166 @@
+"""GPU: the FCN and its companion passes for ANY model the reference's nll
+accepts (VERDICT r01 "what's missing" 1, 2, 5): closures, compositions,
+observable arity 2, six components -- through the parametric functor program
+(interpreter and NVRTC-specialised), against the reference's own values
+frozen in tests/golden (make_golden.py add_generic_models), 1e-10.  Plus the
+reference's error precedence (zero divisor vs non-positive density) and the
+row-sharded FCN's NCCL path (one-rank group) against the one-pass value."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests.golden.generic_models import GENERIC_POINTS, generic_models
+
+pytestmark = pytest.mark.gpu
+
+
+def _stores(hk, arrays):
+    s1 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g1_x"]])
+    s2 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0", "x1"), [arrays["g2_x"], arrays["g2_y"]])
+    s6 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g6_x"]])
+    return {"g1": (s1, ["x0"]), "g2": (s2, ["x0", "x1"]), "g6": (s6, ["x0"])}
+
+
+@pytest.mark.parametrize("jit", ["interpreter", "specialised"])
+def test_generic_models_nll_vs_reference(cuda, hk, golden, jit):
+    from paper_1711_05683_b200 import _lib
+    arrays, scalars = golden
+    gen = scalars["generic"]
+    stores = _stores(hk, arrays)
+    mode = _lib.JIT_OFF if jit == "interpreter" else _lib.JIT_ALWAYS
+    with _lib.jit_mode(mode):
+        for i, pt in enumerate(GENERIC_POINTS):
+            models = generic_models(hk, np, pt)
+            for name in ("g1", "g2", "g6"):
+                store, cols = stores[name]
+                got = hk.nll(models[name], store, cols)
+                assert got == pytest.approx(gen[name][i], rel=1e-10), (name, i)
+
+
+def test_generic_program_compiles_once_per_structure(cuda, hk, golden):
+    """Parameter changes reuse the specialised FCN module: the constants are
+    kernel arguments, only a new op structure compiles."""
+    from paper_1711_05683_b200 import _lib
+    arrays, scalars = golden
+    store, cols = _stores(hk, arrays)["g1"]
+    L = _lib.lib()
+    with _lib.jit_mode(_lib.JIT_ALWAYS):
+        models = generic_models(hk, np, GENERIC_POINTS[0])
+        m = models["g1"]
+        hk.nll(m, store, cols)
+        c0 = L.hk_jit_count()
+        ps = m.param_set()
+        vals = []
+        for k in range(6):
+            ps["m0"].set(0.89 + 0.002 * k)
+            ps["g"].set(0.045 + 0.001 * k)
+            ps["n_bw"].set(3000.0 + 10 * k)
+            vals.append(hk.nll(m, store, cols))
+        assert L.hk_jit_count() == c0
+    assert len(set(vals)) == len(vals)
+    with _lib.jit_mode(_lib.JIT_OFF):
+        assert hk.nll(m, store, cols) == pytest.approx(vals[-1], rel=1e-14)
+
+
+def test_generic_yield_sums_vs_reference(cuda, hk, golden):
+    """Yield stationarity (fitting.py:401-434) for the six-component model
+    (above the old four-component device limit) against the reference."""
+    from paper_1711_05683_b200.fitting import _yield_stationarity
+    arrays, scalars = golden
+    store, cols = _stores(hk, arrays)["g6"]
+    for i, pt in enumerate(GENERIC_POINTS):
+        model = generic_models(hk, np, pt)["g6"]
+        g, A = _yield_stationarity(model, store, cols)
+        want = scalars["generic"]["g6_yields"][i]
+        np.testing.assert_allclose(g + 1.0, np.asarray(want["g"]) + 1.0, rtol=1e-10, atol=0)
+        np.testing.assert_allclose(A, np.asarray(want["A"]), rtol=1e-10, atol=0)
+
+
+def test_generic_splot_identities(cuda, hk, golden):
+    """sPlot on a generic model: after the yield polish the species weights
+    of each event sum to one and each species' weights sum to its yield
+    (splot.py:1-15), through the program-driven kernels."""
+    from paper_1711_05683_b200.fitting import _polish_yields
+    arrays, _ = golden
+    store, cols = _stores(hk, arrays)["g1"]
+    model = generic_models(hk, np, dict(GENERIC_POINTS[0], n_bw=11500.0, n_poly=800.0))["g1"]
+    for y in model.yields():
+        y.lower = 0.0
+    _polish_yields(model, store, cols, 1)
+    g, _ = __import__("paper_1711_05683_b200.fitting", fromlist=["x"])._yield_stationarity(model, store, cols)
+    assert np.max(np.abs(g)) < 1e-9
+    V = hk.splot_matrix(model, store, cols)
+    sw = hk.splot_weights(model, store, cols, V)
+    w = np.stack([np.asarray(sw.column(c)) for c in sw.schema.names])
+    np.testing.assert_allclose(w.sum(axis=0), 1.0, rtol=0, atol=1e-9)
+    yields = [y.value for y in model.yields()]
+    np.testing.assert_allclose(w.sum(axis=1), yields, rtol=1e-8)
+
+
+def test_generic_error_precedence(cuda, hk):
+    """A zero divisor in an expression-tree division raises EvaluationError
+    with the point (functors.py:200-207); a closure's numpy division does
+    not raise -- its inf density is reported as not positive
+    (fitting.py:200-205); the earliest 65536-row batch wins."""
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    x = np.linspace(0.5, 9.5, 200_000)
+    x[150_000] = 3.0                                   # batch 2
+    x[70_000] = 7.0                                    # batch 1
+    store = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    c = P("c", 3.0)
+    tree = hk.combine("/", hk.constant(1.0), hk.combine("-", hk.identity(), hk.wrap_closure(lambda v, p: p["c"].value + 0.0 * v[0], [c])))
+    m1 = hk.add_pdfs([P("n", 1.0)], [hk.make_pdf(tree * tree, lambda r: 1.0, region)])
+    with pytest.raises(hk.EvaluationError, match=r"division by zero at point \(np.float64\(3.0\),\)"):
+        hk.nll(m1, store, ["x0"])
+    clos = hk.wrap_closure(lambda v, p: 1.0 / (v[0] - 7.0) ** 2, [])
+    m2 = hk.add_pdfs([P("n2", 1.0)], [hk.make_pdf(clos, lambda r: 1.0, region)])
+    with pytest.raises(ValueError, match=r"model density np.float64\(inf\) is not positive at event 70000"):
+        hk.nll(m2, store, ["x0"])
+    both = hk.add_pdfs([P("a", 1.0), P("b", 1.0)], [hk.make_pdf(tree * tree, lambda r: 1.0, region),
+                                                    hk.make_pdf(clos, lambda r: 1.0, region)])
+    with pytest.raises(ValueError, match="is not positive at event 70000"):   # batch 1 before batch 2
+        hk.nll(both, store, ["x0"])
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_sharded_nll_nccl_path_one_rank(cuda, hk, golden):
+    """parallel.sharded_nll's device path -- asynchronous FCN pass, NCCL
+    all-gather of the 8-double record, hk_nll_combine publishing into the
+    mapped mailbox -- on a one-rank NCCL group equals nll(), for the closed
+    form and a generic model, and reports a bad event by its global row."""
+    import torch
+    import torch.distributed as dist
+    from paper_1711_05683_b200 import parallel
+    arrays, _ = golden
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        x = arrays["nll_x"]
+        P = hk.Parameter
+        region = hk.BoundedRegion(((0.0, 10.0),))
+        g, e = hk.shape_gaussian(P("mean", 5.0), P("sigma", 0.5)), hk.shape_exponential(P("tau", 3.0))
+        toy = hk.add_pdfs([P("n_sig", 4000.0), P("n_bkg", 6000.0)],
+                          [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+        data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+        assert parallel.sharded_nll(toy, data, ["x0"], 0, _force_collective=True) == hk.nll(toy, data, ["x0"])
+        store, cols = _stores(hk, arrays)["g2"]
+        g2 = generic_models(hk, np, GENERIC_POINTS[1])["g2"]
+        assert parallel.sharded_nll(g2, store, cols, 0, _force_collective=True) == hk.nll(g2, store, cols)
+        bad = x.copy()
+        bad[[2500, 700]] = np.nan
+        bstore = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [bad])
+        with pytest.raises(ValueError, match=r"not positive at event 1000700"):
+            parallel.sharded_nll(toy, bstore, ["x0"], 1_000_000, _force_collective=True)
+    finally:
+        dist.destroy_process_group()

@@ -558,9 +558,13 @@ def test_row_sharded_nll(cuda, hk, oracle, world):
         parts = []
         for r in range(world):
             shard, a = parallel.shard_rows(store, r, world)
-            logsum, first, val = nll_event_sum(model, shard, ["x0"])
-            parts.append((logsum, -1.0 if first is None else float(a + first),
-                          0.0 if val is None else float(val)))
+            logsum, problem = nll_event_sum(model, shard, ["x0"])
+            rec = np.zeros(parallel._PART + 1)
+            rec[0], rec[1] = logsum, -1.0
+            if problem is not None:
+                row, kind, payload = problem
+                rec[1], rec[2], rec[3], rec[-1] = a + row, kind, float(payload), 1
+            parts.append(rec)
         return parallel.combine_nll_parts(parts, model.expected_total())
 
     got = sharded(data)

@@ -31,7 +31,7 @@ def test_cases_cover_every_opcode(hk):
     seen = set()
     for _, prog in _programs(hk):
         seen.update(prog.op[i] for i in range(prog.n_ops))
-    assert seen == set(range(_lib.OP_COL, _lib.OP_SQUARE + 1)), sorted(seen)
+    assert seen == set(range(_lib.OP_COL, _lib.OP_UDIV + 1)), sorted(seen)
 
 
 def test_emitted_source_is_straight_line(hk):
