@@ -392,6 +392,34 @@ int hk_splot_weights_program(const double* const* d_obs, int64_t n, const hk_den
  * the sum's grouping (not its value beyond rounding) depends on the SM count. */
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream);
+/* The FCN at k parameter points in one pass over the data (the numeric
+ * Hessian's 2n^2+1 points, a simplex's initial vertices -- fitting.py:251-395
+ * call the FCN serially): h_logsums[p], h_first_bad[p] as hk_nll_eval would
+ * return for models[p], bit for bit.  The factored Gaussian + exponential
+ * model runs as one kernel (CTA = 4096-row tile x group of 4 points); other
+ * models run one hk_nll_eval per point.  d_work: hk_nll_many_work_doubles(n,
+ * k) doubles, zero-filled before first use.  Synchronous. */
+#define HK_MAX_POINTS 64
+int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int32_t k, double* d_work,
+                     double* h_logsums, uint64_t* h_first_bad, void* stream);
+int64_t hk_nll_many_work_doubles(int64_t n, int32_t k);
+
+/* Resident FCN session (a minimiser's serial FCN calls, fitting.py:251-340,
+ * without a kernel launch per call): hk_fcn_session_start binds the data
+ * column and a zero-filled hk_nll_work_doubles(n) workspace and launches
+ * persistent CTAs (one per SM slot, cooperative launch) on a library stream;
+ * hk_fcn_session_eval(model) posts the parameter point into mapped host
+ * memory and waits for the answer -- the same value as hk_nll_eval, bit for
+ * bit.  Gaussian + exponential models only (HK_EUNSUPPORTED otherwise).  The
+ * CTAs occupy the GPU: other kernels wait until hk_fcn_session_stop, or until
+ * idle_us without a command passes (the next eval relaunches them).  One
+ * session per host thread, on the device current at start. */
+int hk_fcn_session_start(const double* d_x, int64_t n, double* d_work, int64_t idle_us);
+int hk_fcn_session_eval(const hk_model_t* model, double* h_logsum, uint64_t* h_first_bad);
+int hk_fcn_session_stop(void);
+/* diagnostics: device-side ns from command pickup to answer, last session eval */
+int64_t hk_fcn_session_device_ns(void);
+
 /* workspace size of hk_nll_eval / hk_nll_program_eval for n rows (8 + one
  * partial per scheduled CTA) */
 int64_t hk_nll_work_doubles(int64_t n);

@@ -23,6 +23,7 @@ HK_MAX_DAUGHTERS = 16
 HK_MAX_PROGRAM = 256
 HK_MAX_SLOTS = 32
 HK_MAX_COMPONENTS = 8
+HK_MAX_POINTS = 64
 HK_NO_BAD_ROW = (1 << 64) - 1
 HK_RNG_REFERENCE, HK_RNG_PHILOX = 0, 1
 HK_SHAPE_GAUSS, HK_SHAPE_EXPO = 0, 1
@@ -45,6 +46,8 @@ EXPORTS = (
     "hk_init", "hk_shutdown", "hk_clique_size", "hk_allreduce_partials", "hk_allgather_partials",
     "hk_fold_supers", "hk_philox4x32_10",
     "hk_nll_program_eval", "hk_ratio_partials_program", "hk_splot_weights_program", "hk_nll_combine",
+    "hk_nll_eval_many", "hk_nll_many_work_doubles",
+    "hk_fcn_session_start", "hk_fcn_session_eval", "hk_fcn_session_stop", "hk_fcn_session_device_ns",
 )
 
 
@@ -137,6 +140,12 @@ _SIGS = {
     "hk_nll_program_eval": (_INT, [_PP, _I64, _DM, _P, _PD, _PU, _PU, _P]),
     "hk_ratio_partials_program": (_INT, [_PP, _I64, _DM, _P, _P, _P]),
     "hk_nll_combine": (_INT, [_P, _I32, _PD, _PU, _PU, _P]),
+    "hk_nll_eval_many": (_INT, [_P, _I64, _M, _I32, _P, _PD, _PU, _P]),
+    "hk_nll_many_work_doubles": (_I64, [_I64, _I32]),
+    "hk_fcn_session_start": (_INT, [_P, _I64, _P, _I64]),
+    "hk_fcn_session_eval": (_INT, [_M, _PD, _PU]),
+    "hk_fcn_session_stop": (_INT, []),
+    "hk_fcn_session_device_ns": (_I64, []),
     "hk_splot_weights_program": (_INT, [_PP, _I64, _DM, _PD, _PP, _P, _P]),
     "hk_model_density": (_INT, [_P, _I64, _M, _P, _P]),
     "hk_yield_partials": (_INT, [_P, _I64, _M, _P, _P, _P]),

@@ -17,6 +17,9 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "hepkit_cuda.h"
 #include "hk_device.cuh"
@@ -32,8 +35,20 @@ struct Coeffs {
   double shift[HK_MAX_COMPONENTS];  // gauss: mean
   double scale[HK_MAX_COMPONENTS];  // gauss: 1/sigma; expo: -1/tau
   // factored Gaussian+exponential path (kFcnFactored): exponents M inside
-  // (m_lo, m_hi) give amp_k e^M a normal, finite double for both k
+  // (m_lo, m_hi) give amp_k e^M a normal, finite double for both k; q2, q1,
+  // q0: A - B as a quadratic in x - mean
   double m_lo, m_hi;
+  double q2, q1, q0;
+};
+
+// One parameter point of the factored Gaussian + exponential density, for
+// the multi-point pass (hk_nll_eval_many): the fields the factored and
+// reference-order paths read, under Coeffs' names so the same templates
+// produce the same bits.
+struct FPoint {
+  double amp[2], shift[1], scale[2];
+  double m_lo, m_hi;
+  double q2, q1, q0;
 };
 
 // FCN kernel variants
@@ -64,7 +79,8 @@ __device__ __forceinline__ double density(const Coeffs& c, double x) {
 
 // Two-component Gaussian + exponential specialisation (the benchmark model,
 // cli.py:316-320 / toymodel.py): no component loop, no kind branches.
-__device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
+template <class C>
+__device__ __forceinline__ double density_ge(const C& c, double x) {
   const double z = (x - c.shift[0]) * c.scale[0];
   return c.amp[0] * fcn_exp(-0.5 * z * z) + c.amp[1] * fcn_exp(x * c.scale[1]);
 }
@@ -80,23 +96,78 @@ __device__ __forceinline__ double density_ge(const Coeffs& c, double x) {
 // sum, so inside the window t = e^(min-max) is in [0, 1] and s lies in
 // [min amp, amp0 + amp1]: positive and finite, no separate check.  A NaN or
 // infinite x makes M NaN or infinite and fails the window.
-__device__ __forceinline__ bool density_factored(const Coeffs& c, double x, double* s, double* M) {
+// e^v for v <= 0 on the factored path: 2^(v log2 e) = 2^n 2^f with
+// n = rint(v log2 e), f in [-1/2, 1/2] and 2^f a degree-9 polynomial (fitted
+// by reweighted least squares; 1.9e-14 relative on the interval), n added to
+// the exponent field.  13 FP64 instructions against ~17 for libdevice's exp;
+// relative error <= ~1e-13, dominated by the rounding of v log2 e.  Summed
+// over 1e7 events that moves ln L by <= 1e-6 absolute, ~1e-14 relative --
+// the FCN's budget is 1e-10.  v < -707 returns 0 (the host admits the
+// factored path only for amplitude ratios below 1e200, so the dropped term
+// is < 1e-100 of the density).
+__device__ __forceinline__ double fcn_exp_neg(double v) {
+  const double y = v * 1.4426950408889634;          // log2(e)
+  const double magic = 6755399441055744.0;          // 1.5 * 2^52: rounds y to an integer
+  const double r = y + magic;
+  const double f = y - (r - magic);
+  double p = 1.0155003747016481e-07;
+  p = fma(p, f, 1.3259339489411853e-06);
+  p = fma(p, f, 1.5252960462935984e-05);
+  p = fma(p, f, 1.5403435240126103e-04);
+  p = fma(p, f, 1.3333557659884130e-03);
+  p = fma(p, f, 9.6181291916688500e-03);
+  p = fma(p, f, 5.5504108668414306e-02);
+  p = fma(p, f, 2.4022650695651396e-01);
+  p = fma(p, f, 6.9314718055987630e-01);
+  p = fma(p, f, 1.0000000000000115e+00);
+  const long long n = (long long)__double2loint(r);  // the low word of r is rint(y)
+  const double e = __longlong_as_double(__double_as_longlong(p) + (n << 52));
+  return v < -707.0 ? 0.0 : e;
+}
+
+// The factored density d = e^M s with one exponential per event:
+//   A = -z^2/2, z = (x - mean)/sigma; B = -x/tau; M = max(A, B);
+//   t = e^-|A - B|; s = amp_big + amp_small t.
+// (HK_FCN_EXP_POLY: q = A - B as a quadratic in u = x - mean,
+//   (q2 u + q1) u + q0 with q2 = -1/(2 sigma^2), q1 = 1/tau, q0 = mean/tau,
+//   M = B + max(q, 0), t = fcn_exp_neg(-|q|).)
+// Returns false (the caller falls back to the reference-order density_ge and
+// its positivity check) unless M is inside the window where both terms are
+// finite normal doubles; a NaN x fails the window.  Against the reference op
+// order each event's density moves by a few 1e-13 relative.
+//
+// Measured on B200 (tools/fcn_kernel_time.py, 1e7 events): the quadratic +
+// fcn_exp_neg form (HK_FCN_EXP_POLY) saves ~4 FP64 instructions per event but
+// needs more registers -- one-point pass 31.1 vs 32.2 us, the multi-point
+// kernel 32.7 vs 28.8 us per point (spills at 64 registers) -- so the
+// default is the libdevice form below.
+template <class C>
+__device__ __forceinline__ bool density_factored(const C& c, double x, double* s, double* M) {
+#ifndef HK_FCN_EXP_POLY  // libdevice exp, A and B separately
   const double z = (x - c.shift[0]) * c.scale[0];
   const double A = -0.5 * z * z;
   const double B = x * c.scale[1];
-  // (fmax(A, B) and exp(-|A - B|) instead of the selects measured slower:
-  // 29.8 vs 29.0 us per 1e7 events)
-  const bool ga = A >= B;  // NaN: false, M = B = NaN
-  *M = ga ? A : B;
-  const double t = fcn_exp(ga ? B - A : A - B);
-  *s = ga ? c.amp[0] + c.amp[1] * t : c.amp[0] * t + c.amp[1];
+  const bool ga0 = A >= B;
+  *M = ga0 ? A : B;
+  const double t0 = fcn_exp(ga0 ? B - A : A - B);
+  *s = ga0 ? c.amp[0] + c.amp[1] * t0 : c.amp[0] * t0 + c.amp[1];
   return *M > c.m_lo && *M < c.m_hi;
+#else
+  const double u = x - c.shift[0];
+  const double q = fma(fma(c.q2, u, c.q1), u, c.q0);
+  const double B = x * c.scale[1];
+  const bool ga = q >= 0.0;  // NaN: false, M = B + ... = NaN
+  *M = ga ? B + q : B;
+  const double t = fcn_exp_neg(ga ? -q : q);
+  *s = ga ? fma(c.amp[1], t, c.amp[0]) : fma(c.amp[0], t, c.amp[1]);
+  return *M > c.m_lo && *M < c.m_hi;
+#endif
 }
 
 // One tile: returns sum ln d over this thread's rows; flags
 // d <= 0 / non-finite (fitting.py:200-205) as ~row in *bad (max = first row).
-template <int V>
-__device__ __forceinline__ void fcn_row(const Coeffs& c, double xv, int64_t row, LogProd& lp,
+template <int V, class C>
+__device__ __forceinline__ void fcn_row(const C& c, double xv, int64_t row, LogProd& lp,
                                        double& msum, unsigned long long* bad) {
   if (V == kFcnFactored) {
     double s, M;
@@ -106,18 +177,24 @@ __device__ __forceinline__ void fcn_row(const Coeffs& c, double xv, int64_t row,
       return;
     }
   }
-  const double d = V == kFcnGeneric ? density(c, xv) : density_ge(c, xv);
+  double d;
+  if constexpr (V == kFcnGeneric)
+    d = density(c, xv);
+  else
+    d = density_ge(c, xv);
   if (!(d > 0.0) || !isfinite(d)) *bad = max(*bad, ~(unsigned long long)row);
   lp.add(d);
 }
 
 // sum ln d over rows [begin, end) (at most one tile): all 16 loads in flight
 // for a full tile, a guarded loop otherwise
-template <int V>
+// tid: the thread's slot in the tile (threadIdx.x, or a warp-scheduled
+// virtual id in the resident session -- same rows, same order)
+template <int V, class C>
 __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int64_t begin,
-                                               int64_t end, const Coeffs& c,
-                                               unsigned long long* bad) {
-  const int64_t r0 = begin + threadIdx.x;
+                                               int64_t end, const C& c,
+                                               unsigned long long* bad, int tid) {
+  const int64_t r0 = begin + tid;
   LogProd lp;
   double msum = 0.0;
   if (end - begin == kFcnTile) {
@@ -140,7 +217,7 @@ __device__ __forceinline__ double chunk_logsum(const double* __restrict__ x, int
                                                const Coeffs& c, int64_t ch,
                                                unsigned long long* bad) {
   const int64_t b = ch * kFcnTile;
-  return range_logsum<V>(x, b, b + kFcnTile < n ? b + kFcnTile : n, c, bad);
+  return range_logsum<V>(x, b, b + kFcnTile < n ? b + kFcnTile : n, c, bad, threadIdx.x);
 }
 
 template <int V>
@@ -175,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const d
     unsigned long long bad = 0;
     int64_t begin, end;
     fcn_range(w, n, ch, &begin, &end);
-    double acc[1] = {range_logsum<V>(x, begin, end, c, &bad)};
+    double acc[1] = {range_logsum<V>(x, begin, end, c, &bad, threadIdx.x)};
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
@@ -257,6 +334,385 @@ __global__ void __launch_bounds__(kBlock) k_yield(const double* __restrict__ x, 
   }
 }
 
+// ---------------------------------------------------- multi-point FCN -----
+// K parameter points of the factored Gaussian + exponential model in one
+// pass over the data (hk_nll_eval_many): CTA (tile t, group g) evaluates the
+// tile for points 4g .. 4g+3 from one register copy of its 16 rows per
+// thread, so a Hessian's 51 points (fitting.py:365-386) read the column once
+// per group instead of once per call, and the grid is tiles x groups CTAs
+// (many waves: no ramp/tail per point).  Per point the arithmetic, the tile
+// partials and the fold are those of k_nll_fused (same templates, same
+// order), so each value is bit-identical to a single-point hk_nll_eval.
+#ifndef HK_FCN_MANY_G
+#define HK_FCN_MANY_G 2
+#endif
+constexpr int kManyG = HK_FCN_MANY_G;
+// 3 CTAs/SM (80 registers): the 16 register-resident rows live across the
+// four points' passes; at 64 registers they spill
+#ifndef HK_FCN_MANY_MIN_BLOCKS
+#define HK_FCN_MANY_MIN_BLOCKS 4
+#endif
+
+struct ManyArgs {
+  const double* x;
+  int64_t n;
+  int32_t k, groups;
+  int64_t tiles, kpad;
+  double* part;                  // [tile][kpad]
+  double* out;                   // [k] sums
+  unsigned long long* bad;       // [k] ~first bad row, 0 = none
+  unsigned int* gticket;         // [groups] tiles finished per group
+  unsigned int* done;            // groups folded
+  volatile unsigned long long* host_mail;
+  unsigned long long seq;
+  FPoint pt[HK_MAX_POINTS];  // k points, padded with copies of the last to kpad
+};
+
+__global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(const __grid_constant__ ManyArgs a) {
+  __shared__ unsigned int s_t;
+  __shared__ double tot[kManyG];
+  const int64_t total = a.tiles * a.groups;
+  for (int64_t b = blockIdx.x; b < total; b += gridDim.x) {
+    const int64_t t = b % a.tiles;
+    const int g = (int)(b / a.tiles);
+    const int64_t begin = t * kFcnTile;
+    const int64_t end = begin + kFcnTile < a.n ? begin + kFcnTile : a.n;
+    const int64_t r0 = begin + threadIdx.x;
+    const bool full = end - begin == kFcnTile;
+    // the group's four points advance together, row by row: four independent
+    // LogProd / exponent-sum chains per thread (ILP 4); per point the row
+    // order -- and so every rounding -- is that of range_logsum
+    LogProd lp[kManyG];
+    double msum[kManyG];
+    unsigned long long bad[kManyG];
+#pragma unroll
+    for (int j = 0; j < kManyG; ++j) {
+      msum[j] = 0.0;
+      bad[j] = 0;
+    }
+    const FPoint* c = a.pt + g * kManyG;  // padded to kpad points on the host
+    if (full) {
+      double xv[kFcnRows];
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(a.x + r0 + i * kBlock);
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) {
+#pragma unroll
+        for (int j = 0; j < kManyG; ++j)
+          fcn_row<kFcnFactored>(c[j], xv[i], r0 + i * kBlock, lp[j], msum[j], &bad[j]);
+      }
+    } else {
+      for (int i = 0; i < kFcnRows; ++i) {  // the ragged last tile, as range_logsum
+        const int64_t r = r0 + i * kBlock;
+        if (r >= end) continue;
+        const double xr = __ldg(a.x + r);
+#pragma unroll
+        for (int j = 0; j < kManyG; ++j) fcn_row<kFcnFactored>(c[j], xr, r, lp[j], msum[j], &bad[j]);
+      }
+    }
+    double acc[kManyG];
+#pragma unroll
+    for (int j = 0; j < kManyG; ++j) {
+      acc[j] = lp[j].value() + msum[j];
+      if (bad[j] && g * kManyG + j < a.k) atomicMax(a.bad + g * kManyG + j, bad[j]);
+    }
+    block_sum_store<kManyG>(acc, a.part + t * a.kpad + g * kManyG);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_t = atomicAdd(a.gticket + g, 1u);
+    }
+    __syncthreads();
+    if (s_t != a.tiles - 1) continue;
+    // last tile of group g: fold its points in k_nll_fused's order, publish
+    __threadfence();
+    double f[kManyG];
+#pragma unroll
+    for (int j = 0; j < kManyG; ++j) f[j] = 0.0;
+    for (int64_t i = threadIdx.x; i < a.tiles; i += kBlock) {
+#pragma unroll
+      for (int j = 0; j < kManyG; ++j) f[j] += __ldcg(a.part + i * a.kpad + g * kManyG + j);
+    }
+    block_sum_store<kManyG>(f, tot);
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < kManyG; ++j) {
+        const int p = g * kManyG + j;
+        if (p >= a.k) break;
+        const unsigned long long bb = atomicExch(a.bad + p, 0ull);
+        a.out[p] = tot[j];
+        if (a.host_mail) {
+          a.host_mail[1 + p] = (unsigned long long)__double_as_longlong(tot[j]);
+          a.host_mail[1 + a.k + p] = ~bb;
+        }
+      }
+      a.gticket[g] = 0u;
+      __threadfence_system();
+      if (atomicAdd(a.done, 1u) == (unsigned)a.groups - 1) {
+        *a.done = 0u;
+        __threadfence_system();
+        if (a.host_mail) a.host_mail[0] = a.seq;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ resident FCN session ----
+// A minimiser calls the FCN serially (fitting.py:251-340), so each call pays
+// a kernel launch plus the launch's ramp (measured on B200: 10.4 us launch +
+// mapped-memory signal round trip, tools/launch_latency.cu) on top of the
+// ~25 us of arithmetic.  A session keeps one persistent CTA per slot
+// (SMs x 4, co-resident by cooperative launch) waiting on a command word in
+// mapped host memory: the host writes the parameter point and a sequence
+// number; CTA 0 sees it (one PCIe read, ~3.4 us round trip in total),
+// publishes it in device memory, every CTA runs the same tiles as
+// k_nll_fused (same arithmetic, same partials, same last-CTA fold -- values
+// bit-identical to hk_nll_eval) and the last CTA answers through the mailbox.
+// The CTAs leave when told to, or after an idle timeout (the host relaunches
+// on the next call), so a forgotten session cannot hold the GPU.
+// Command page in mapped host memory: kCmdSlots 16-byte slots {seq, word},
+// each written by the host with one aligned 16-byte store (atomic on x86
+// with AVX), read by lanes 0..10 of CTA 0's first warp with one 16-byte load
+// each -- 11 concurrent PCIe reads per poll, and a command is taken only when
+// every slot carries the same new seq, so no ordering between the reads is
+// needed.  Words: 0 = variant | stop << 8, 1..10 = the FPoint.
+constexpr int kCmdSlots = 11;
+struct alignas(16) CmdSlot {
+  unsigned long long seq;
+  unsigned long long word;
+};
+struct ServerCmd {
+  CmdSlot slot[kCmdSlots];
+};
+
+struct ServerDev {          // device memory
+  unsigned long long gen;   // current command seq; ~0 = leave
+  unsigned long long done;  // last seq answered
+  unsigned long long next;  // dynamic tile counter of the current command
+  long long t_seen;         // globaltimer when CTA 0 took the command (diagnostics)
+  int32_t variant, _pad;
+  FPoint c;
+};
+
+struct ServerArgs {
+  const double* x;
+  int64_t n;
+  FcnWork w;                // out/bad/ticket/part of the session workspace; host_mail
+  const ServerCmd* cmd;     // device view of the mapped command page
+  ServerDev* dev;
+  long long idle_ns;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void ld_slot_sys(const CmdSlot* p, unsigned long long* seq, unsigned long long* word) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(*seq), "=l"(*word) : "l"(p) : "memory");
+}
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// CTA 0, warp 0: wait for a complete new command (or the idle timeout), copy
+// it to device memory and release it to every CTA through dev->gen.
+__device__ __forceinline__ void server_poll(const ServerArgs& a, unsigned long long mine) {
+  const int lane = threadIdx.x & 31;
+  const long long t0 = global_ns();
+  unsigned long long s = 0, word = 0;
+  for (;;) {
+    if (lane < kCmdSlots) ld_slot_sys(&a.cmd->slot[lane], &s, &word);
+    const unsigned long long s0 = __shfl_sync(0xffffffffu, s, 0);
+    const bool same = __all_sync(0xffffffffu, lane >= kCmdSlots || s == s0);
+    if (same && s0 != mine) {
+      s = s0;
+      break;
+    }
+    if (global_ns() - t0 > a.idle_ns) {
+      s = ~0ull;
+      break;
+    }
+  }
+  const unsigned long long w0 = __shfl_sync(0xffffffffu, word, 0);
+  if (s != ~0ull && (w0 >> 8)) s = ~0ull;  // stop
+  if (s != ~0ull && lane >= 1 && lane < kCmdSlots) {
+    double* c = &a.dev->c.amp[0];           // FPoint: 10 consecutive doubles
+    c[lane - 1] = __longlong_as_double((long long)word);
+  }
+  if (lane == 0) {
+    if (s != ~0ull) {
+      a.dev->variant = (int32_t)(w0 & 0xff);
+      a.dev->next = 0ull;
+      a.dev->t_seen = global_ns();
+    } else {
+      a.w.host_mail[6] = 1ull;  // left (idle timeout or stop): the host relaunches before the next command
+    }
+    __threadfence();
+  }
+  __syncwarp();
+  if (lane == 0) st_release_gpu(&a.dev->gen, s);
+}
+
+template <int V>
+__device__ __forceinline__ void server_tile(const ServerArgs& a, const FPoint& c, int64_t ch) {
+  unsigned long long bad = 0;
+  int64_t begin, end;
+  fcn_range(a.w, a.n, ch, &begin, &end);
+  double acc[1] = {range_logsum<V>(a.x, begin, end, c, &bad, threadIdx.x)};
+  if (bad) atomicMax(a.w.bad, bad);
+  block_sum_store<1>(acc, a.w.part + ch);
+}
+
+template <int V>
+__device__ __forceinline__ void server_tiles(const ServerArgs& a, const FPoint& c, int64_t chunks) {
+  // dynamic tiles (like a launch's block scheduler): the 74 tiles past
+  // 4 x 592 of a 1e7-event set go to the CTAs that finish first (static
+  // rounds measured slower); tile ch's partial is the same value whichever
+  // CTA computes it.  The next index is fetched while the current tile
+  // computes, so the atomic's latency hides.
+  __shared__ long long s_tile;
+  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(&a.dev->next, 1ull);
+  __syncthreads();
+  int64_t ch = s_tile;
+  while (ch < chunks) {
+    __syncthreads();  // every thread has read s_tile
+    unsigned long long nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(&a.dev->next, 1ull);
+    server_tile<V>(a, c, ch);
+    if (threadIdx.x == 0) s_tile = (long long)nxt;
+    __syncthreads();
+    ch = s_tile;
+  }
+}
+
+#ifndef HK_FCN_SERVER_MIN_BLOCKS
+#define HK_FCN_SERVER_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kBlock, HK_FCN_SERVER_MIN_BLOCKS) k_fcn_server(const __grid_constant__ ServerArgs a) {
+  __shared__ unsigned long long s_gen;
+  __shared__ FPoint s_c;
+  __shared__ int s_variant;
+  unsigned long long mine = a.dev->done;
+  const int64_t chunks = a.w.full + a.w.tail_ctas;
+  for (;;) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) server_poll(a, mine);
+    if (threadIdx.x == 0) {
+      // waiters back off: a spinning warp would take issue slots from the
+      // CTAs still computing on the same SM
+      unsigned long long g;
+      while ((g = ld_acquire_gpu(&a.dev->gen)) == mine) __nanosleep(32);
+      s_gen = g;
+      if (g != ~0ull) {
+        s_variant = a.dev->variant;
+        s_c = a.dev->c;
+      }
+    }
+    __syncthreads();
+    const unsigned long long g = s_gen;
+    if (g == ~0ull) return;
+    mine = g;
+    // the coefficients stay in shared memory (operands are LDS'd where the
+    // arithmetic needs them): a register copy costs 14 of the 64 registers
+    if (s_variant == kFcnFactored)
+      server_tiles<kFcnFactored>(a, s_c, chunks);
+    else
+      server_tiles<kFcnGE>(a, s_c, chunks);
+    // fcn_finish with this command's sequence number
+    __shared__ unsigned int s_ticket;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_ticket = atomicAdd(a.w.ticket, 1u);
+    }
+    __syncthreads();
+    if (s_ticket == gridDim.x - 1) {
+      __threadfence();
+      double acc[1] = {0.0};
+      for (int64_t i = threadIdx.x; i < chunks; i += kBlock) acc[0] += __ldcg(a.w.part + i);
+      __shared__ double total;
+      block_sum_store<1>(acc, &total);
+      if (threadIdx.x == 0) {
+        a.dev->done = g;
+        a.w.host_mail[4] = (unsigned long long)a.dev->t_seen;  // device-side span of the command
+        a.w.host_mail[5] = (unsigned long long)global_ns();
+        FcnWork w = a.w;
+        w.seq = g;
+        fcn_publish(w, total);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct Session {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  ServerCmd* h_cmd = nullptr;       // mapped
+  ServerCmd* d_cmd = nullptr;
+  ServerDev* dev = nullptr;
+  ServerArgs args{};
+  unsigned grid = 0;
+  bool running = false;
+  unsigned long long seq = 0;
+};
+thread_local Session t_session;
+
+// one aligned 16-byte store per slot (SSE2 movdqa: atomic on AVX-capable
+// x86 hosts), so the device never sees a slot's seq without its word
+void write_slots(ServerCmd* h, const CmdSlot* v) {
+  std::atomic_thread_fence(std::memory_order_release);
+  for (int k = 0; k < kCmdSlots; ++k) {
+#if defined(__SSE2__)
+    _mm_store_si128(reinterpret_cast<__m128i*>(&h->slot[k]),
+                    _mm_set_epi64x((long long)v[k].word, (long long)v[k].seq));
+#else
+    __atomic_store(reinterpret_cast<__int128*>(&h->slot[k]), reinterpret_cast<const __int128*>(&v[k]),
+                   __ATOMIC_RELEASE);
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+}
+
+int session_launch(Session& S) {
+  // the next command must be seen as new: gen = done = last answered seq
+  ServerDev init{};
+  init.gen = init.done = S.seq;
+  HK_CUDA(cudaMemcpyAsync(S.dev, &init, sizeof(init), cudaMemcpyHostToDevice, S.stream));
+  void* params[] = {&S.args};
+  HK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_fcn_server), dim3(S.grid), dim3(kBlock),
+                                      params, 0, S.stream));
+  S.running = true;
+  return HK_OK;
+}
+
+int session_stop(Session& S) {
+  if (S.device < 0) return HK_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(S.device);
+  if (S.running && cudaStreamQuery(S.stream) == cudaErrorNotReady) {
+    CmdSlot v[kCmdSlots];
+    const unsigned long long seq = S.seq + 0x100000000ull;  // any seq the server has not answered
+    for (int k = 0; k < kCmdSlots; ++k) {
+      v[k].seq = seq;
+      v[k].word = k == 0 ? (1ull << 8) : 0ull;
+    }
+    write_slots(S.h_cmd, v);
+  }
+  const cudaError_t e = cudaStreamSynchronize(S.stream);
+  cudaStreamDestroy(S.stream);
+  cudaFreeHost(S.h_cmd);
+  cudaFree(S.dev);
+  cudaSetDevice(cur);
+  S = Session{};
+  if (e != cudaSuccess) return cuda_fail(e, "hk_fcn_session_stop");
+  return HK_OK;
+}
+
 int make_coeffs(const hk_model_t* m, Coeffs* c) {
   HK_REQUIRE(m != nullptr, "NULL model");
   HK_REQUIRE(m->n_comp >= 1 && m->n_comp <= HK_MAX_COMPONENTS, "component count %d outside 1..%d",
@@ -284,9 +740,14 @@ int make_coeffs(const hk_model_t* m, Coeffs* c) {
   c->m_lo = 0.0;
   c->m_hi = -1.0;  // empty: variant kFcnFactored not applicable
   if (m->n_comp == 2 && c->amp[0] > 1e-250 && c->amp[1] > 1e-250 && c->amp[0] < 1e300 &&
-      c->amp[1] < 1e300) {
+      c->amp[1] < 1e300 && std::fmax(c->amp[0], c->amp[1]) < 1e200 * std::fmin(c->amp[0], c->amp[1])) {
     c->m_lo = -690.0 - std::log(std::fmin(c->amp[0], c->amp[1]));
     c->m_hi = 700.0 - std::log(c->amp[0] + c->amp[1]);
+  }
+  if (m->n_comp == 2 && m->kind[0] == HK_SHAPE_GAUSS && m->kind[1] == HK_SHAPE_EXPO) {
+    c->q2 = -0.5 * c->scale[0] * c->scale[0];
+    c->q1 = -c->scale[1];
+    c->q0 = -c->shift[0] * c->scale[1];
   }
   return HK_OK;
 }
@@ -373,8 +834,11 @@ __global__ void __launch_bounds__(kBlock) k_splot(const double* __restrict__ x, 
   }
 }
 
-// Mapped pinned mailbox per (host thread, device) for hk_nll_eval:
-// [0] sequence number, [1] sum-of-logs bits, [2] first bad row.
+// Mapped pinned mailbox per (host thread, device) for the FCN entry points:
+// [0] sequence number, then the payload -- [1] sum-of-logs bits, [2] first
+// bad row, [3] first zero divisor for one point; [1..k] sums and [k+1..2k]
+// first bad rows for the k points of hk_nll_eval_many.
+constexpr int kMailWords = 1 + 2 * HK_MAX_POINTS;
 struct Mailbox {
   volatile unsigned long long* h = nullptr;  // host view
   unsigned long long* d = nullptr;           // device view of the same memory
@@ -390,8 +854,8 @@ int mailbox(Mailbox** out) {
   Mailbox& m = t_boxes[dev & 15];
   if (m.device != dev) {
     void* p = nullptr;
-    HK_CUDA(cudaHostAlloc(&p, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
-    std::memset(p, 0, 4 * sizeof(unsigned long long));
+    HK_CUDA(cudaHostAlloc(&p, kMailWords * sizeof(unsigned long long), cudaHostAllocMapped));
+    std::memset(p, 0, kMailWords * sizeof(unsigned long long));
     void* dp = nullptr;
     HK_CUDA(cudaHostGetDevicePointer(&dp, p, 0));
     m.h = static_cast<volatile unsigned long long*>(p);
@@ -405,6 +869,7 @@ int mailbox(Mailbox** out) {
 
 // hk_shutdown: free this thread's mailboxes (rebuilt by the next hk_nll_eval)
 void fcn_release() {
+  session_stop(t_session);
   for (Mailbox& m : t_boxes) {
     if (m.device < 0) continue;
     cudaFreeHost(const_cast<unsigned long long*>(m.h));
@@ -766,6 +1231,176 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   if (int rc = check_launch("k_nll_fused")) return rc;
   if (!h_logsum) return HK_OK;
   return fcn_wait(mb, w.seq, st, "hk_nll_eval", h_logsum, h_first_bad, nullptr);
+}
+
+int64_t hk_nll_many_work_doubles(int64_t n, int32_t k) {
+  const int64_t groups = k < 1 ? 1 : (k + kManyG - 1) / kManyG;
+  return 256 + (n <= 0 ? 0 : (n + kFcnTile - 1) / kFcnTile) * groups * kManyG;
+}
+
+int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int32_t k, double* d_work,
+                     double* h_logsums, uint64_t* h_first_bad, void* stream) {
+  HK_REQUIRE(k >= 1 && k <= HK_MAX_POINTS, "point count %d outside 1..%d", k, HK_MAX_POINTS);
+  HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
+  HK_REQUIRE(d_x && d_work && models && h_logsums && h_first_bad, "NULL pointer");
+  ManyArgs a;
+  std::memset(&a, 0, sizeof(a));
+  bool factored = true;
+  for (int p = 0; p < k; ++p) {
+    Coeffs c;
+    if (int rc = make_coeffs(models + p, &c)) return rc;
+    if (fcn_variant(c) != kFcnFactored) {
+      factored = false;
+      break;
+    }
+    a.pt[p].amp[0] = c.amp[0];
+    a.pt[p].amp[1] = c.amp[1];
+    a.pt[p].shift[0] = c.shift[0];
+    a.pt[p].scale[0] = c.scale[0];
+    a.pt[p].scale[1] = c.scale[1];
+    a.pt[p].m_lo = c.m_lo;
+    a.pt[p].m_hi = c.m_hi;
+    a.pt[p].q2 = c.q2;
+    a.pt[p].q1 = c.q1;
+    a.pt[p].q0 = c.q0;
+  }
+  for (int p = k; p < ((k + kManyG - 1) / kManyG) * kManyG; ++p) a.pt[p] = a.pt[k - 1];
+  if (!factored) {  // other model kinds: one single-point pass per point (same values)
+    int64_t full, tail;
+    fcn_schedule(n, &full, &tail);
+    for (int p = 0; p < k; ++p)
+      if (int rc = hk_nll_eval(d_x, n, models + p, d_work, h_logsums + p, h_first_bad + p, stream)) return rc;
+    return HK_OK;
+  }
+  // d_work (zero-filled once, re-armed by the kernel): [0, 64) sums,
+  // [64, 128) ~bad cells, [128, 160) group tickets (u32), [160] done (u32),
+  // [256 ..) partials [tile][kpad]
+  a.x = d_x;
+  a.n = n;
+  a.k = k;
+  a.groups = (k + kManyG - 1) / kManyG;
+  a.tiles = (n + kFcnTile - 1) / kFcnTile;
+  a.kpad = (int64_t)a.groups * kManyG;
+  a.out = d_work;
+  a.bad = reinterpret_cast<unsigned long long*>(d_work + 64);
+  a.gticket = reinterpret_cast<unsigned int*>(d_work + 128);
+  a.done = reinterpret_cast<unsigned int*>(d_work + 160);
+  a.part = d_work + 256;
+  Mailbox* mb = nullptr;
+  if (int rc = mailbox(&mb)) return rc;
+  a.host_mail = mb->d;
+  a.seq = ++mb->seq;
+  cudaStream_t st = as_stream(stream);
+  k_nll_many<<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);
+  if (int rc = check_launch("k_nll_many")) return rc;
+  double first = 0.0;
+  uint64_t dummy = 0;
+  // fcn_wait reads [1], [2]; the payload here is [1 .. 2k]
+  if (int rc = fcn_wait(mb, a.seq, st, "hk_nll_eval_many", &first, &dummy, nullptr)) return rc;
+  for (int p = 0; p < k; ++p) {
+    const unsigned long long bits = mb->h[1 + p];
+    std::memcpy(h_logsums + p, &bits, sizeof(double));
+    h_first_bad[p] = mb->h[1 + k + p];
+  }
+  return HK_OK;
+}
+
+int hk_fcn_session_start(const double* d_x, int64_t n, double* d_work, int64_t idle_us) {
+  HK_REQUIRE(n > 0 && d_x && d_work, "bad session arguments");
+  HK_REQUIRE(idle_us > 0, "idle timeout must be positive");
+  if (int rc = session_stop(t_session)) return rc;
+  Session& S = t_session;
+  int dev = 0, sms = 0, per_sm = 0, coop = 0;
+  HK_CUDA(cudaGetDevice(&dev));
+  HK_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  HK_REQUIRE(coop, "device %d has no cooperative launch", dev);
+  HK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  HK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fcn_server, kBlock, 0));
+  HK_REQUIRE(per_sm >= 1, "FCN session kernel does not fit an SM");
+  S.device = dev;
+  HK_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+  HK_CUDA(cudaHostAlloc(&S.h_cmd, sizeof(ServerCmd), cudaHostAllocMapped));
+  std::memset(S.h_cmd, 0, sizeof(ServerCmd));
+  HK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.d_cmd), S.h_cmd, 0));
+  HK_CUDA(cudaMalloc(&S.dev, sizeof(ServerDev)));
+  Mailbox* mb = nullptr;
+  if (int rc = mailbox(&mb)) return rc;
+  FcnWork w;
+  if (int rc = fcn_setup(d_work, n, &w, nullptr)) return rc;
+  w.div0 = nullptr;
+  w.host_mail = mb->d;
+  S.args.x = d_x;
+  S.args.n = n;
+  S.args.w = w;
+  S.args.cmd = S.d_cmd;
+  S.args.dev = S.dev;
+  S.args.idle_ns = idle_us * 1000;
+  S.grid = (unsigned)(sms * per_sm);
+  mb->h[6] = 0;
+  return session_launch(S);
+}
+
+int hk_fcn_session_eval(const hk_model_t* model, double* h_logsum, uint64_t* h_first_bad) {
+  Session& S = t_session;
+  HK_REQUIRE(S.device >= 0, "no FCN session on this thread (hk_fcn_session_start)");
+  HK_REQUIRE(h_logsum && h_first_bad, "NULL pointer");
+  Coeffs c;
+  if (int rc = make_coeffs(model, &c)) return rc;
+  const int variant = fcn_variant(c);
+  if (variant == kFcnGeneric) {
+    set_error("an FCN session serves the Gaussian + exponential model");
+    return HK_EUNSUPPORTED;
+  }
+  int cur = 0;
+  HK_CUDA(cudaGetDevice(&cur));
+  HK_REQUIRE(cur == S.device, "FCN session lives on device %d, current device is %d", S.device, cur);
+  Mailbox* mb = nullptr;
+  if (int rc = mailbox(&mb)) return rc;
+  if (mb->h[6]) {  // the CTAs left on their idle timeout: bring them back
+    HK_CUDA(cudaStreamSynchronize(S.stream));
+    mb->h[6] = 0;
+    if (int rc = session_launch(S)) return rc;
+  }
+  // the mailbox's sequence numbers are per (thread, device): the session's
+  // command seq is the mailbox seq the answer will carry
+  const unsigned long long seq = ++mb->seq;
+  const double words[kCmdSlots - 1] = {c.amp[0], c.amp[1], c.shift[0], c.scale[0], c.scale[1],
+                                       c.m_lo,   c.m_hi,   c.q2,       c.q1,       c.q0};
+  CmdSlot v[kCmdSlots];
+  v[0].seq = seq;
+  v[0].word = (unsigned long long)variant;
+  for (int k = 1; k < kCmdSlots; ++k) {
+    v[k].seq = seq;
+    std::memcpy(&v[k].word, &words[k - 1], 8);
+  }
+  write_slots(S.h_cmd, v);
+  for (unsigned spins = 1;; ++spins) {
+    if (mb->h[0] == seq) break;
+    if ((spins & 4095u) == 0) {
+      const cudaError_t e = cudaStreamQuery(S.stream);
+      if (e == cudaSuccess) {  // timed out between our check and the command: relaunch
+        if (mb->h[0] == seq) break;
+        mb->h[6] = 0;
+        if (int rc = session_launch(S)) return rc;
+      } else if (e != cudaErrorNotReady) {
+        return cuda_fail(e, "hk_fcn_session_eval");
+      }
+    }
+  }
+  S.seq = seq;  // answered: a relaunch must treat it as done
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const unsigned long long sum_bits = mb->h[1];
+  std::memcpy(h_logsum, &sum_bits, sizeof(double));
+  *h_first_bad = mb->h[2];
+  return HK_OK;
+}
+
+int hk_fcn_session_stop(void) { return session_stop(t_session); }
+
+int64_t hk_fcn_session_device_ns(void) {
+  Mailbox* mb = nullptr;
+  if (mailbox(&mb)) return -1;
+  return (int64_t)(mb->h[5] - mb->h[4]);
 }
 
 int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,

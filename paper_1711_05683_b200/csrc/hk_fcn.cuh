@@ -4,7 +4,9 @@
 // embeds this header), so every variant reduces in the same order:
 //
 //   per HK_FCN_TILE = 4096-row tile: 16 rows per thread, sum ln d as
-//   ln(prod d) (LogProd), a fixed CTA tree -> one partial per tile;
+//   ln(prod d) (LogProd), a fixed CTA tree -> one partial per tile (per-warp
+//   partials without the tile barrier measured slower: the last CTA's fold
+//   of 8x the partials costs more than the barrier stalls it removes);
 //   the last CTA to finish folds the tile partials in a fixed order,
 //   publishes (sum, first bad row, first zero divisor) -- optionally into
 //   mapped pinned host memory -- and re-arms the workspace.

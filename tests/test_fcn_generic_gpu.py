@@ -164,3 +164,133 @@ def test_sharded_nll_nccl_path_one_rank(cuda, hk, golden):
             parallel.sharded_nll(toy, bstore, ["x0"], 1_000_000, _force_collective=True)
     finally:
         dist.destroy_process_group()
+
+
+def _toy_model(hk, n_sig=4000.0, n_bkg=6000.0):
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(P("mean", 5.0, step=0.1), P("sigma", 0.5, step=0.05, lower=1e-4))
+    e = hk.shape_exponential(P("tau", 3.0, step=0.2, lower=1e-4))
+    return hk.add_pdfs([P("n_sig", n_sig, step=60.0, lower=0.0), P("n_bkg", n_bkg, step=80.0, lower=0.0)],
+                       [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 51, 70])
+def test_nll_many_bitwise_equals_serial(cuda, hk, golden, k):
+    """fitting.nll_many (hk_nll_eval_many: one data pass for all points) is
+    bit-identical to k serial nll() calls, ragged tile included, and a bad
+    point raises the serial path's error for the first such point."""
+    from paper_1711_05683_b200.fitting import nll_many
+    arrays, _ = golden
+    x = np.concatenate([arrays["nll_x"], arrays["nll_x"][:777]])
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    model = _toy_model(hk)
+    ps = model.param_set()
+    rs = np.random.default_rng(k)
+    base = np.array(ps.values())
+    pts = [tuple(base * (1.0 + 0.02 * rs.standard_normal(len(base)))) for _ in range(k)]
+    got = nll_many(model, data, ["x0"], pts)
+    assert ps.values() == tuple(base)
+    want = []
+    for pt in pts:
+        ps.set_values(pt)
+        want.append(hk.nll(model, data, ["x0"]))
+    ps.set_values(tuple(base))
+    assert np.array_equal(np.array(got), np.array(want))
+    # generic model: per-point device passes, same values as serial
+    g1 = generic_models(hk, np, GENERIC_POINTS[0])["g1"]
+    s1 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g1_x"]])
+    p1 = g1.param_set()
+    b1 = p1.values()
+    gp = [b1, tuple(v * 1.01 for v in b1)]
+    gv = nll_many(g1, s1, ["x0"], gp)
+    p1.set_values(gp[1])
+    assert gv[1] == hk.nll(g1, s1, ["x0"])
+    p1.set_values(b1)
+    # a NaN observable: every point's density fails there; the first point's
+    # error is raised, as by the serial evaluation
+    xb = x.copy()
+    xb[9000] = np.nan
+    bdata = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [xb])
+    with pytest.raises(ValueError) as want:
+        ps.set_values(pts[0])
+        hk.nll(model, bdata, ["x0"])
+    ps.set_values(tuple(base))
+    with pytest.raises(ValueError) as got_exc:
+        nll_many(model, bdata, ["x0"], pts)
+    assert str(got_exc.value) == str(want.value) == "model density np.float64(nan) is not positive at event 9000"
+    assert ps.values() == tuple(base)
+
+
+def test_fit_batched_objective_identical_to_serial(cuda, hk, golden):
+    """fit() through NllObjective (batched simplex vertices and Hessian) ends
+    at exactly the parameters, errors and call count of the serial objective
+    (fitting.py:477-513), and numeric_errors gives the same errors bitwise."""
+    from paper_1711_05683_b200.fitting import NllObjective, minimize, numeric_errors
+    arrays, _ = golden
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["nll_x"]])
+    m1, m2 = _toy_model(hk), _toy_model(hk)
+    for m in (m1, m2):
+        ps = m.param_set()
+        ps["mean"].set(4.8)
+        ps["sigma"].set(0.6)
+        ps["tau"].set(2.5)
+    r1 = minimize(NllObjective(m1, data, ["x0"]), m1.param_set())
+    r2 = minimize(lambda _p: hk.nll(m2, data, ["x0"]), m2.param_set())
+    assert r1.status == r2.status and r1.n_calls == r2.n_calls and r1.nll_min == r2.nll_min
+    assert m1.param_set().values() == m2.param_set().values()
+    assert r1.errors == r2.errors
+    e1 = numeric_errors(NllObjective(m1, data, ["x0"]), m1.param_set())
+    e2 = numeric_errors(lambda _p: hk.nll(m2, data, ["x0"]), m2.param_set())
+    assert e1 == e2
+    res = hk.fit(m1, data, ["x0"])
+    assert res.status is hk.FitStatus.CONVERGED
+
+
+def test_fcn_session_bitwise_and_lifecycle(cuda, hk, golden):
+    """fcn_session: nll() through the resident CTAs equals the launched path
+    bit for bit across changing parameters; the CTAs leave on idle and come
+    back on the next call; a bad event stops the session and raises the
+    reference error; other GPU work runs after the block."""
+    import time
+    from paper_1711_05683_b200 import _lib
+    arrays, _ = golden
+    x = np.concatenate([arrays["nll_x"]] * 3)[:29_999]
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    model = _toy_model(hk, 12000.0, 18000.0)
+    ps = model.param_set()
+    pts = [(4000.0 * 3, 5.0, 0.5, 18000.0, 3.0), (12100.0, 4.9, 0.55, 17900.0, 2.8)]
+    want = []
+    for pt in pts:
+        ps.set_values(pt)
+        want.append(hk.nll(model, data, ["x0"]))
+    with hk.fcn_session(model, data, ["x0"], idle_ms=20.0) as s:
+        assert s.on
+        got = []
+        for i in range(10):
+            ps.set_values(pts[i % 2])
+            got.append(hk.nll(model, data, ["x0"]))
+        assert got == [want[i % 2] for i in range(10)]
+        time.sleep(0.1)                      # the CTAs leave on their idle timeout ...
+        ps.set_values(pts[1])
+        assert hk.nll(model, data, ["x0"]) == want[1]   # ... and come back
+    assert not s.on
+    t = cuda.ones(10, device="cuda")
+    assert float(t.sum()) == 10.0
+    bad = x.copy()
+    bad[777] = np.nan
+    bdata = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [bad])
+    with pytest.raises(ValueError) as want_exc:
+        hk.nll(model, bdata, ["x0"])
+    with hk.fcn_session(model, bdata, ["x0"]) as s2:
+        with pytest.raises(ValueError) as got_exc:
+            hk.nll(model, bdata, ["x0"])
+        assert not s2.on
+    assert str(got_exc.value) == str(want_exc.value)
+    # a generic model opens no session and keeps the launched path
+    g1 = generic_models(hk, np, GENERIC_POINTS[0])["g1"]
+    s1 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g1_x"]])
+    with hk.fcn_session(g1, s1, ["x0"]) as s3:
+        assert not s3.on
+        assert hk.nll(g1, s1, ["x0"]) == pytest.approx(-116014.30412842518, rel=1e-10)
+    assert _lib.lib().hk_fcn_session_stop() == 0
