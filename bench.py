@@ -34,6 +34,7 @@ M_B0, DAUGHTERS = 5.27966, (3.0969, 0.493677, 0.13957039)
 EVENTS_PER_GPU = 100_000_000
 BYTES_PER_EVENT = 8 * (4 * 3 + 1)          # algorithmic HBM bytes written per 3-body event
 FCN_EVENTS = 10_000_000
+WORKLOAD = "C2: B0->J/psi K pi phase-space generation + weight sum/mean/variance, 1e8 events/GPU in HBM"
 
 
 def _peaks() -> dict:
@@ -70,7 +71,7 @@ def _fp64_roofline(kernel: str, events_per_s_per_gpu: float, note: str = "") -> 
             "unit": "T DP inst/s", "frac": inst / pk["dp_inst_per_s"],
             "tflops": events_per_s_per_gpu * k["dp_flops_per_event"] * 1e-12, "peak_tflops": pk["tflops"],
             "dp_inst_per_event": k["dp_inst_per_event"],
-            "source": "per-event DP counts: profiles/r01_fp64_roofline.json (ncu); peak: " + pk["source"],
+            "source": "DP inst/event: ncu (profiles/r01_fp64_roofline.json); peak: tools/fp64_peak.cu",
             **({"note": note} if note else {})}
 
 
@@ -188,52 +189,124 @@ class ClockSampler:
                 "samples": len(rows), "reasons": reasons}
 
 
-def cpu_reference(steps: int, warmup: int, sample: int | None = None) -> dict:
-    """The reference algorithm on the host cores: bit-exact C port of
-    phsp_generate + numpy weight integration, all threads."""
+def bench_config(events_per_gpu: int, events_per_step: int) -> dict:
+    """The workload both arms run (identical dicts for the same --gpus)."""
+    return {"workload": WORKLOAD, "events_per_gpu": events_per_gpu, "events_per_step": events_per_step,
+            "decay": "B0(5.27966) -> J/psi(3.0969) K(0.493677) pi(0.13957039), mother at rest, RngKey(1,1)",
+            "rng": "reference SplitMix64 stream (bit-exact to the reference)",
+            "l2": "each step writes 104 B/event (10.4 GB per GPU >> 126 MB L2): no flush needed"}
+
+
+def _best_of(fn, reps: int) -> float:
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def _reference_python():
+    """The reference package itself, installed offline into baseline/_ref
+    (`pip install --no-index --no-deps --target baseline/_ref /root/reference/pkg`;
+    git-ignored, travels to the GPU box with the snapshot).  None when absent."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "hepkit")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)      # appended: never shadows the drop-in package
+    try:
+        import hepkit
+    except Exception:  # noqa: BLE001 -- a broken install is reported as absent
+        return None
+    return hepkit
+
+
+def cpu_reference(reps: int = 3) -> dict:
+    """CPU baseline of C2 (generation + weight sum / mean / variance) on this
+    box's host cores: best-of-`reps` wall clock at 1
+    thread and at os.cpu_count() threads, for
+      * the reference's own Python (`hepkit.phsp_generate(..., workers=w)` +
+        numpy weight sums) from baseline/_ref, when installed;
+      * the bit-exact C port of the same algorithm (oracle/, -ffp-contract=off,
+        pthreads) -- the headline `value` (the faster of the two CPU paths).
+    Bounded samples (rates, not the full 1e8): ~10-30 s of CPU work in all."""
     import numpy as np
 
     from oracle import oracle as O  # the CPU baseline leg (test/bench infrastructure only)
 
-    threads = os.cpu_count() or 1
-    if sample is None:
-        t0 = time.perf_counter()
-        O.generate(DAUGHTERS, M_B0, 1_000_000, 1, 1, threads=threads)
-        rate = 1_000_000 / (time.perf_counter() - t0)
-        sample = int(min(max(rate * 3.0, 1_000_000), 50_000_000))   # ~3 s per step
-    times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        cols = O.generate(DAUGHTERS, M_B0, sample, 1, 1, ev_begin=i * sample, threads=threads)
-        w = cols["weight"]
-        _ = (float(np.sum(w)), float(np.sum(w * w)))
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-        del cols, w
-    t = statistics.median(times)
-    return {"value": sample / t, "unit": "events/s", "cores": threads, "kind": "port",
-            "sample": f"{sample} B0->J/psi K pi events + weight sums per step (C oracle port, "
-                      f"-ffp-contract=off, {threads} pthreads), median of {steps}",
-            "seconds_per_step": t}
+    cores = os.cpu_count() or 1
+
+    def port(n, threads):
+        def run():
+            w = O.generate(DAUGHTERS, M_B0, n, 1, 1, threads=threads)["weight"]
+            return float(np.sum(w)), float(np.sum(w * w))
+        return n / _best_of(run, reps)
+
+    out = {"unit": "events/s", "cores": cores, "kind": "port", "best_of": reps}
+    n_port = 50_000_000 if cores >= 8 else 10_000_000
+    out["value"] = port(n_port, cores)
+    out["port_1_thread"] = port(5_000_000, 1)
+    ref = _reference_python()
+    rp = None
+    if ref is not None:
+        spec, mother = ref.DecaySpec(M_B0, DAUGHTERS), ref.FourVector.at_rest(M_B0)
+        rp = {"source": "baseline/_ref hepkit (the unmodified reference)", "events": 1_000_000}
+        for workers in (1, cores):
+            def run(workers=workers):
+                blk = ref.phsp_generate(spec, mother, 1_000_000, ref.RngKey(1, 1), workers=workers)
+                w = np.asarray(blk.column("weight"))
+                return float(np.sum(w)), float(np.sum(w * w))
+            rp[f"workers_{workers}"] = 1_000_000 / _best_of(run, reps)
+    out["reference_python"] = rp if rp else "baseline/_ref not installed on this box"
+    out["sample"] = (f"C2 rate: port {n_port} events at {cores} threads and 5e6 at 1 thread; reference Python "
+                     f"1e6 events at workers=1 and {cores}; best of {reps}")
+    return out
 
 
 def run_reference(args) -> None:
+    """The reference arm: the reference algorithm's CPU implementation (the
+    bit-exact C port, all host threads) on the SAME workload as our arm --
+    1e8 events per GPU of our arm generated + weight sum/mean/variance per
+    step -- in slices of 2.5e7 rows (global rows, so the events and weights
+    are those of one call over the whole step) to bound host memory."""
+    import numpy as np
+
+    from oracle import oracle as O  # reference arm (bench infrastructure only)
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    base = cpu_reference(args.steps, args.warmup)
+    cores = os.cpu_count() or 1
+    n, sl = EVENTS_PER_GPU * args.gpus, 25_000_000    # our arm's whole-job step: 1e8 events per GPU
+
+    def step():
+        s = s2 = 0.0
+        for b in range(0, n, sl):
+            w = O.generate(DAUGHTERS, M_B0, sl, 1, 1, ev_begin=b, threads=cores)["weight"]
+            s += float(np.sum(w))
+            s2 += float(np.sum(w * w))
+        return s, s2
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s, s2 = step()
+    per = (time.perf_counter() - t0) / args.steps
+    value = n / per
     line = {
-        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "events/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": base["seconds_per_step"] * 1e3, "higher_is_better": True,
+        "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: B0->J/psi K pi 3-body generation + weight integration "
-                               "(bounded CPU sample per step)", "events_per_step": None},
-        "cpu_baseline": base,
-        "e2e": {"value": base["value"], "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": bench_config(EVENTS_PER_GPU, n),
+        "result": {"weight_sum": s, "weight_mean": s / n, "weight_variance": max(s2 / n - (s / n) ** 2, 0.0)},
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": cores, "kind": "port",
+                         "sample": f"the full {n:.0e}-event step (2.5e7-row slices), C oracle port, "
+                                   f"{cores} pthreads, mean of {args.steps} steps"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    line["config"]["events_per_step"] = int(round(base["value"] * base["seconds_per_step"]))
     print(json.dumps(line), flush=True)
 
 
@@ -306,18 +379,76 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
         _lib.lib().hk_nll_eval(_lib.ptr(x), n_local, lm, _lib.ptr(work), ctypes.byref(logsum),
                                ctypes.byref(first), st.cuda_stream)
     ct = max_over_ranks((time.perf_counter() - c0) / evals)
-    return {"metric": "FCN evals/s @1e7 events (gauss+exp extended NLL, fp64)", "value": 1.0 / dt,
-            "unit": "evals/s", "n_gpus": world, "scaling": "strong", "us_per_eval": dt * 1e6,
-            "kernel_us_per_eval": kt * 1e6, "c_abi_us_per_eval": ct * 1e6,
-            "kernel_events_per_s": FCN_EVENTS / kt, "evals": evals,
-            "roofline": _fp64_roofline("k_nll_fused", n_local / kt,
-                                       "rate from kernel_us_per_eval (k_nll<factored>, back to back); DP counts "
-                                       "of the API's k_nll_fused<2>, the same per-event arithmetic plus the "
-                                       "last-CTA fold"),
-            "timing": "CUDA events around the eval loop on each rank's stream (each eval ends with the value "
-                      "on the host), max over ranks",
-            "parallelism": f"row shards of {n_local} events per GPU, rank-order fold of per-rank log-sums",
-            "data": "1e7 events from generate_model_sample(build_model(scale=200), RngKey(7,2), poisson=False) on device"}
+    out = {"metric": "FCN evals/s @1e7 events (gauss+exp extended NLL, fp64)", "value": 1.0 / dt,
+           "unit": "evals/s", "n_gpus": world, "scaling": "strong", "us_per_eval": dt * 1e6,
+           "kernel_us": kt * 1e6, "c_abi_us": ct * 1e6,
+           "roofline": _fp64_roofline("k_nll_fused", n_local / kt)}
+    if world == 1:
+        out.update(fcn_minimiser_paths(hk, torch, model, data, points, (mean, sigma, tau), evals))
+    return out
+
+
+def fcn_minimiser_paths(hk, torch, model, data, points, pars, evals: int) -> dict:
+    """The two FCN paths a fit uses besides plain nll(): the resident FCN
+    session that fit() opens around the simplex (serial calls, no launch per
+    call) and the batched multi-point pass (nll_many: numeric_errors' 51
+    Hessian points in one data pass); plus the whole C4 fit's wall time from
+    a displaced start (simplex + yield polish + errors)."""
+    from paper_1711_05683_b200.fitting import nll_many
+
+    mean, sigma, tau = pars
+    res = {}
+    with hk.fcn_session(model, data, ["x0"]):
+        def one(i):
+            p = points[i % 2]
+            mean.set(p[0]); sigma.set(p[1]); tau.set(p[2])
+            return hk.nll(model, data, ["x0"])
+        for i in range(10):
+            one(i)
+        t0 = time.perf_counter()
+        for i in range(evals):
+            one(i)
+        res["session_evals_per_s"] = evals / (time.perf_counter() - t0)
+    ps = model.param_set()
+    base = ps.values()
+    import numpy as np
+    rs = np.random.default_rng(1)
+    pts = [tuple(np.asarray(base) * (1 + 1e-4 * rs.standard_normal(len(base)))) for _ in range(51)]
+    nll_many(model, data, ["x0"], pts)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        nll_many(model, data, ["x0"], pts)
+    res["batched51_evals_per_s"] = 51 * 10 / (time.perf_counter() - t0)
+    saved = ps.values()
+    ps["mean"].set(4.8); ps["sigma"].set(0.6); ps["tau"].set(2.6)
+    t0 = time.perf_counter()
+    fr = hk.fit(model, data, ["x0"])
+    res["fit_s"] = time.perf_counter() - t0
+    res["fit_calls"] = fr.n_calls
+    res["fit_status"] = fr.status.value
+    ps.set_values(saved)
+    return res
+
+
+def write_only_peak(torch) -> float:
+    """HBM write-only bandwidth measured live on this GPU: torch fill_ of a
+    4 GiB fp64 buffer (>> L2), best of 10, CUDA events -- the north_star's
+    "HBM-write roofline" denominator beside MEASURED_PEAKS.json's copy BW."""
+    buf = torch.empty(1 << 29, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        buf.fill_(1.0)
+    best = 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(10):
+        e0.record()
+        buf.fill_(float(i))
+        e1.record()
+        e1.synchronize()
+        best = max(best, buf.numel() * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del buf
+    torch.cuda.empty_cache()
+    return best
 
 
 def _timed(torch, fn, reps: int, dist=None) -> float:
@@ -363,8 +494,27 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         return blk.meta["weight_partials"]
 
     dt = _timed(torch, c1, 50, dist)
-    out["C1"] = {"workload": "1e5 B0->J/psi K pi events per GPU, phsp_generate API (device store)",
-                 "value": world * n1 / dt, "unit": "events/s", "ms_per_call": dt * 1e3}
+    out["C1"] = {"what": "1e5 events/GPU, phsp_generate API", "value": world * n1 / dt, "ms": dt * 1e3}
+    # C2 on the production stream (Philox4x32-10): the same kernel launch as the
+    # headline step, device-timed, 104 B/event written
+    peak = _peaks()["hbm_gbs"]
+    d = _lib.make_decay(spec, mother, M_B0)
+    kp = _lib.make_key(hk.RngKey(1, 1), hk.rng.rng_mode("philox"))
+    n2 = EVENTS_PER_GPU
+    cols = [_lib.empty(n2) for _ in range(13)]
+    colp = _lib.ptr_array(cols)
+    wp = _lib.empty(2 * _lib.num_weight_slices(n2))
+    st = torch.cuda.current_stream()
+
+    def c2p():
+        _lib.check(_lib.lib().hk_phsp_generate(d, kp, rank * n2, n2, colp, _lib.ptr(wp), st.cuda_stream), "philox")
+
+    dt = _timed(torch, c2p, 10, dist)
+    out["C2_philox"] = {"what": "C2 generator on the Philox4x32-10 production stream, 1e8 events/GPU",
+                        "value": world * n2 / dt, "ms": dt * 1e3, "GBps": BYTES_PER_EVENT * n2 / dt / 1e9,
+                        "frac_copy": BYTES_PER_EVENT * n2 / dt / 1e9 / peak}
+    del cols, colp, wp
+    torch.cuda.empty_cache()
     # C3: fused generate + J/psi -> mu mu chain, 4-body final state, 136 B/event
     n3 = 125_000_000
     sub = hk.DecaySpec(3.0969, (0.1056583755, 0.1056583755))
@@ -376,10 +526,9 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     c3()
     torch.cuda.empty_cache()
     dt = _timed(torch, c3, 5, dist)
-    peak = _peaks()["hbm_gbs"]
-    out["C3"] = {"workload": "B0->J/psi(->mu mu) K pi fused chain, 1.25e8 events per GPU (1e9 / 8), 17 columns",
-                 "value": world * n3 / dt, "unit": "events/s", "ms_per_step": dt * 1e3,
-                 "hbm_GBps_per_gpu": 136 * n3 / dt / 1e9, "frac_of_measured_copy_bw": 136 * n3 / dt / 1e9 / peak}
+    out["C3"] = {"what": "fused chain B0->J/psi(->mu mu) K pi, 1.25e8 events/GPU, 136 B/event",
+                 "value": world * n3 / dt, "ms": dt * 1e3, "GBps": 136 * n3 / dt / 1e9,
+                 "frac_copy": 136 * n3 / dt / 1e9 / peak}
     torch.cuda.empty_cache()
     # C5: 1e10 events, generation -> m^2_12 -> moments, no store; shards + NCCL gather + fold
 
@@ -399,12 +548,9 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         res["r"] = hk.phsp_average(hk.identity(), blk, m12)
 
     dt = _timed(torch, c2avg, 10, dist)
-    out["C2_average"] = {"workload": "phsp_average(<m12^2>) over a stored 1e8-event block per GPU "
-                                     "(public API, 72 B/event read)",
-                         "value": world * EVENTS_PER_GPU / dt, "unit": "events/s", "ms_per_call": dt * 1e3,
-                         "hbm_GBps_per_gpu": 72 * EVENTS_PER_GPU / dt / 1e9,
-                         "frac_of_measured_copy_bw": 72 * EVENTS_PER_GPU / dt / 1e9 / peak,
-                         "m12sq_average": float(res["r"].value)}
+    out["C2_average"] = {"what": "phsp_average(<m12^2>) over a stored 1e8 block, 72 B/event read",
+                         "value": world * EVENTS_PER_GPU / dt, "ms": dt * 1e3,
+                         "frac_copy": 72 * EVENTS_PER_GPU / dt / 1e9 / peak}
     # CSV: write_csv of 1e7 stored rows, GPU-formatted text streamed to a file
     from paper_1711_05683_b200.store import ColumnStore
     n_csv = 10_000_000
@@ -414,10 +560,8 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         t0 = time.perf_counter()
         sub.write_csv(fh)
         dt = time.perf_counter() - t0
-    out["CSV"] = {"workload": "ColumnStore.write_csv of 1e7 stored 13-column rows (f\"{v:.17g}\" text, "
-                              "formatted on the GPU, streamed through pinned memory to /dev/null)",
-                  "value": n_csv / dt, "unit": "rows/s", "seconds": dt,
-                  "note": "host wall clock: the text leaves the GPU; reference Python body ~1.5e5 rows/s"}
+    out["CSV"] = {"what": "write_csv of 1e7 13-column rows (%.17g on GPU), host wall clock",
+                  "value": n_csv / dt, "unit": "rows/s"}
     del sub
     del blk
     torch.cuda.empty_cache()
@@ -428,11 +572,9 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         res["r"] = sharded_integrate(hk.identity(), spec, mother, n5, hk.RngKey(1, 1), m12)
 
     dt = _timed(torch, c5, 2, dist)
-    out["C5"] = {"workload": "1e10 B0->J/psi K pi events, fused generation + <m12^2> weighted average, "
-                             f"strong scaling over {world} GPU(s), no event store; 1024 super-chunk records "
-                             "(40 KB) cross GPUs",
-                 "value": n5 / dt, "unit": "events/s", "seconds": dt, "m12sq_average": float(res["r"].value),
-                 "roofline": _fp64_roofline("hk_jit_integrate", n5 / dt / world)}
+    rf = _fp64_roofline("hk_jit_integrate", n5 / dt / world)
+    out["C5"] = {"what": "1e10 events, fused generation + <m12^2>, strong scaling, no store",
+                 "value": n5 / dt, "s": dt, "fp64_frac": rf["frac"] if rf else None}
     # C5 secondary integrand: K*(892) Breit-Wigner on m^2_K pi, the named builtin
 
     def m23(cols):
@@ -446,9 +588,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         res["r"] = sharded_integrate(hk.breit_wigner(0.89555, 0.0473), spec, mother, n5, hk.RngKey(1, 1), m23)
 
     dt = _timed(torch, c5bw, 2, dist)
-    out["C5_bw"] = {"workload": "1e10 events, fused generation + <BW_K*(892)(m^2_K pi)> (M=0.89555, G=0.0473), "
-                                f"strong scaling over {world} GPU(s), no event store",
-                    "value": n5 / dt, "unit": "events/s", "seconds": dt, "bw_average": float(res["r"].value)}
+    out["C5_bw"] = {"what": "1e10 events, fused generation + <BW_K*(892)(m^2_K pi)>", "value": n5 / dt}
     # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
     # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
     expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
@@ -461,10 +601,8 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     dt_jit = _timed(torch, c5g, 3, dist)
     with _lib.jit_mode(_lib.JIT_OFF):
         dt_int = _timed(torch, c5g, 1, dist)
-    out["C5_generic"] = {"workload": "1e9 events, fused generation + <m12^2 * BW(m12^2)> (non-Dalitz-pair "
-                                     f"integrand) over {world} GPU(s)",
-                         "value": world * n5g / dt_jit, "unit": "events/s", "seconds": dt_jit,
-                         "interpreter_value": world * n5g / dt_int}
+    out["C5_generic"] = {"what": "1e9 events, <m12^2 * BW(m12^2)> NVRTC kernel (interpreter beside)",
+                         "value": world * n5g / dt_jit, "interpreter": world * n5g / dt_int}
     return out
 
 
@@ -543,11 +681,12 @@ def run_ours(args) -> None:
     achieved = BYTES_PER_EVENT * n / gen_avg / 1e9
     traffic = _traffic()
 
+    del cols
+    torch.cuda.empty_cache()
+    write_peak = write_only_peak(torch)
     # end to end through the public API, host buffers (pinned), D2H inside the timed region
     e2e = None
     if rank == 0 or world > 1:
-        del cols
-        torch.cuda.empty_cache()
         # N > 1: 1e8 / N events per rank, so the job pins ~10.4 GB of host
         # memory in total at any N (the leg is PCIe-bound per GPU; the rate
         # does not depend on the per-rank size)
@@ -564,7 +703,7 @@ def run_ours(args) -> None:
                "unit": "events/s", "events_per_rank": n_e,
                "h2d_bytes_per_step": ctypes.sizeof(_lib.hk_decay_t) + ctypes.sizeof(_lib.hk_key_t),
                "d2h_bytes_per_step": BYTES_PER_EVENT * n_e + 16,
-               "api": "phsp_generate_to_host (pinned host columns; generation overlapped with D2H)",
+               "api": "phsp_generate_to_host: pinned host columns, D2H overlapped with generation",
                "steps": e_steps}
         if dist:
             e2e["value"] = world * n_e / _max_over_ranks(torch, dist, e_dt)
@@ -598,31 +737,29 @@ def run_ours(args) -> None:
         a_dt = _max_over_ranks(torch, dist, (time.perf_counter() - a0) / e_steps)
         e2e["api_device_resident"] = {
             "value": n_total / a_dt, "unit": "events/s",
-            "api": "phsp_generate -> phsp_weight_moments (events stay in HBM; result read to host)",
+            "api": "phsp_generate -> phsp_weight_moments, events stay in HBM",
             "d2h_bytes_per_step": 16}
 
     others = None if args.no_configs else other_configs(hk, torch, _lib, rank, world, dist)
     fcn = None if args.no_fcn else fcn_bench(hk, torch, evals=args.fcn_evals, rank=rank, world=world, dist=dist)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference(steps=1, warmup=0)
+        cpu = cpu_reference()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: B0->J/psi K pi 3-body phase-space generation + weight integration "
-                                   "(sum/mean/variance), 1e8 events per GPU, stored to HBM",
-                       "events_per_gpu": n, "events_per_step": n_total, "rng": "reference SplitMix64 stream",
-                       "parallelism": f"dp{world} (contiguous super-chunk-aligned event shards, NCCL all-gather of 1024 super-chunk records)",
-                       "l2": "each step writes 10.4 GB per GPU (> 126 MB L2): no flush needed",
-                       "weight_sum": float(sums[0]), "weight_mean": float(sums[0] / n_total),
+            "config": bench_config(n, n_total),
+            "parallelism": f"dp{world}: contiguous super-chunk-aligned event shards, NCCL all-gather of 1024 super-chunk records",
+            "result": {"weight_sum": float(sums[0]), "weight_mean": float(sums[0] / n_total),
                        "weight_variance": float(max(sums[1] / n_total - (sums[0] / n_total) ** 2, 0.0))},
             "roofline": {"bound": "hbm", "kernel": "k_generate<3, reference>", "achieved": achieved,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "peak_source": peaks["source"], "traffic": traffic,
                          "algorithmic_bytes_per_event": BYTES_PER_EVENT,
-                         "kernel_ms": gen_avg * 1e3, "kernel_share_of_step": gen_avg / per_step},
+                         "kernel_ms": gen_avg * 1e3, "kernel_share_of_step": gen_avg / per_step,
+                         "write_only_peak": write_peak, "frac_vs_write_only": achieved / write_peak},
             "clocks": clocks.summary(),
             "e2e": e2e,
             "gpu_launches": 3 * args.steps,   # k_generate + k_fold_supers + k_fold per step

@@ -469,6 +469,7 @@ __device__ __forceinline__ double rest_event(const hk_decay_t& d, const RngParam
 // (Used for chain sub-decays such as J/psi -> mu mu.)
 struct TwoBody {
   double w, q, r, gamma, g2, e2, m0;
+  double e1;  // sqrt(q^2 + m0^2): daughter 0's rest-frame energy (fixed-frame chain path)
 };
 
 __device__ __forceinline__ TwoBody two_body_consts(const hk_decay_t& d) {
@@ -484,7 +485,59 @@ __device__ __forceinline__ TwoBody two_body_consts(const hk_decay_t& d) {
   t.g2 = t.gamma * t.gamma * fast_rcp(t.gamma + 1.0);
   t.e2 = fast_sqrt(t.q * t.q + d.masses[1] * d.masses[1]);
   t.m0 = d.masses[0];
+  t.e1 = cle;
   return t;
+}
+
+// Lorentz boost into the lab of a frame with four-momentum (fe, P) and FIXED
+// mass m (im = 1/m, rem = 1/(fe + m)): with beta = P/fe and gamma = fe/m,
+//   E' = (fe E + P.p) / m,   p' = p + P ((P.p) / (fe + m) + E) / m,
+// the same transformation as _boost (phasespace.py:74-81) with gamma^2/(gamma+1)
+// (beta.p) beta rewritten through m -- 10 FP64 instructions per daughter and
+// one reciprocal per frame instead of make_frame_fast's three.  Used by the
+// fused chain when the host has proved the frame mass is the decay's (see
+// hk_phsp_generate_chain); rounding differs from _boost's by a few ulp * E.
+struct MFrame {
+  double e, px, py, pz, im, rem;
+};
+
+__device__ __forceinline__ void boost_m(const MFrame& f, double& e, double& px, double& py, double& pz) {
+  const double s = fma(f.px, px, fma(f.py, py, f.pz * pz));
+  const double c = fma(s, f.rem, e) * f.im;
+  e = fma(f.e, e, s) * f.im;
+  px = fma(c, f.px, px);
+  py = fma(c, f.py, py);
+  pz = fma(c, f.pz, pz);
+}
+
+// Two-body decay in the fixed frame f: daughters (e1, q n) and (e2, -q n) in
+// the rest frame (the reference's GENBOD for n = 2 gives daughter 0 as a boost
+// of (m0, 0) to (e1, q n), daughter 1 as (e2, -q n)), boosted together: the
+// shared P.(q n) is computed once.  Same draws and direction as rest_event2.
+template <int MODE>
+__device__ __forceinline__ double two_body_boosted(const TwoBody& t, const RngParams& rp, uint64_t row,
+                                                   const MFrame& f, double (&p)[8]) {
+  uint64_t bits[2];
+  draw_bits<2, MODE>(rp, row, bits);
+  const double cz = two_unit_minus_one(bits[0]);
+  const double two_u = two_unit(bits[1]);
+  const double sz = fast_sqrt(1.0 - cz * cz);
+  double sn, cs;
+  math::k_sincospi(two_u, &sn, &cs);
+  const double qs = t.q * sz;
+  const double cx = qs * cs, cy = qs * sn, czq = t.q * cz;
+  const double s = fma(f.px, cx, fma(f.py, cy, f.pz * czq));
+  const double c0 = fma(s, f.rem, t.e1) * f.im;
+  const double c1 = fma(-s, f.rem, t.e2) * f.im;
+  p[0] = fma(f.e, t.e1, s) * f.im;
+  p[1] = fma(c0, f.px, cx);
+  p[2] = fma(c0, f.py, cy);
+  p[3] = fma(c0, f.pz, czq);
+  p[4] = fma(f.e, t.e2, -s) * f.im;
+  p[5] = fma(c1, f.px, -cx);
+  p[6] = fma(c1, f.py, -cy);
+  p[7] = fma(c1, f.pz, -czq);
+  return t.w;
 }
 
 template <int MODE>

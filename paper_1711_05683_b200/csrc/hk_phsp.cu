@@ -12,6 +12,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 
 #include "hepkit_cuda.h"
@@ -312,6 +313,9 @@ struct GenChainArgs {
   double* cols[kMaxCols];  // spliced schema order
   double* wpart;
   unsigned long long* first_bad;
+  // fixed-frame path (host-proved, see hk_phsp_generate_chain): the decaying
+  // daughter's mass m_k and 1/m_k replace its per-event frame mass
+  double fixed_m, fixed_im;
 };
 
 // Parent daughters other than the decaying one go to their spliced slots.
@@ -340,7 +344,7 @@ __device__ __forceinline__ void store_parent_daughters(const GenChainArgs& a, in
 // test so two calls interleave; a mass mismatch lowers *bad to the row.
 // K >= 0: the decaying daughter as a compile-time index (the hot 3-body
 // parent), so its four-vector is a register reference instead of a select chain.
-template <int N, int NS, int MODE, int K>
+template <int N, int NS, int MODE, int K, bool FIXED>
 __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& mf, const TwoBody& tb,
                                             const RestHoist& hp, int64_t r, unsigned long long* bad) {
   const int k = K >= 0 ? K : a.k;
@@ -369,17 +373,29 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
       fz = select_f64(sel, p[4 * j + 3], fz);
     }
   }
-  const double fm = gen_frame_mass(fe, fx, fy, fz);
-  *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
   double q[4 * NS];
   double ws;
-  if constexpr (NS == 2)
-    ws = rest_event2<MODE>(tb, a.rp_sub, row, q);  // per-launch constants hoisted, same bits
-  else
-    ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
-  const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
+  if constexpr (FIXED) {
+    // frame mass = m_k (host-proved within the tolerance, no per-event check)
+    const MFrame f{fe, fx, fy, fz, a.fixed_im, fast_rcp(fe + a.fixed_m)};
+    if constexpr (NS == 2) {
+      ws = two_body_boosted<MODE>(tb, a.rp_sub, row, f, q);
+    } else {
+      ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
 #pragma unroll
-  for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+      for (int s = 0; s < NS; ++s) boost_m(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+    }
+  } else {
+    const double fm = gen_frame_mass(fe, fx, fy, fz);
+    *bad = mass_mismatch(fm, a.sub.mother_mass) ? min(*bad, (unsigned long long)row) : *bad;
+    if constexpr (NS == 2)
+      ws = rest_event2<MODE>(tb, a.rp_sub, row, q);  // per-launch constants hoisted, same bits
+    else
+      ws = rest_event<NS, MODE>(a.sub, a.rp_sub, row, q);
+    const Frame f = make_frame_fast(fe, fx, fy, fz, fm);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) boost_fma(f, q[4 * s], q[4 * s + 1], q[4 * s + 2], q[4 * s + 3]);
+  }
   const double w = wp * ws;
   __stcs(a.cols[0] + r, w);
   store_parent_daughters<0, N, NS>(a, k, p, r);
@@ -406,7 +422,7 @@ __device__ __forceinline__ double chain_row(const GenChainArgs& a, const Frame& 
 #ifndef HK_CHAIN_T
 #define HK_CHAIN_T 64
 #endif
-template <int N, int NS, int MODE, int K>
+template <int N, int NS, int MODE, int K, bool FIXED>
 __global__ void __launch_bounds__(HK_CHAIN_T, HK_CHAIN_MINB * (kBlock / HK_CHAIN_T))
     k_generate_chain(const __grid_constant__ GenChainArgs a) {
   constexpr int kSplit = kBlock / HK_CHAIN_T;
@@ -426,8 +442,8 @@ __global__ void __launch_bounds__(HK_CHAIN_T, HK_CHAIN_MINB * (kBlock / HK_CHAIN
 #pragma unroll 1
       for (int i = 0; i < kRowsPerThread / 2; ++i) {  // two events per iteration (ILP 2)
         const int64_t r0 = c * HK_CHUNK + i * kBlock + vt;
-        const double w0 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0, &bad);
-        const double w1 = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r0 + HK_CHUNK / 2, &bad);
+        const double w0 = chain_row<N, NS, MODE, K, FIXED>(a, mf, tb, hp, r0, &bad);
+        const double w1 = chain_row<N, NS, MODE, K, FIXED>(a, mf, tb, hp, r0 + HK_CHUNK / 2, &bad);
         acc[0] += w0;
         acc[1] += w0 * w0;
         acc[0] += w1;
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(HK_CHAIN_T, HK_CHAIN_MINB * (kBlock / HK_CHAIN
       for (int i = 0; i < kRowsPerThread; ++i) {
         const int64_t r = c * HK_CHUNK + i * kBlock + vt;
         if (r < a.count) {
-          const double w = chain_row<N, NS, MODE, K>(a, mf, tb, hp, r, &bad);
+          const double w = chain_row<N, NS, MODE, K, FIXED>(a, mf, tb, hp, r, &bad);
           acc[0] += w;
           acc[1] += w * w;
         }
@@ -765,7 +781,10 @@ template <int N, int NS, int MODE>
 void launch_gen_chain(const GenChainArgs& a, unsigned grid, cudaStream_t st) {
   (void)grid;
   const unsigned g = chunk_grid(num_chunks(a.count) * (kBlock / HK_CHAIN_T));
-  k_generate_chain<N, NS, MODE, -1><<<g, HK_CHAIN_T, 0, st>>>(a);
+  if (a.fixed_m > 0.0)
+    k_generate_chain<N, NS, MODE, -1, true><<<g, HK_CHAIN_T, 0, st>>>(a);
+  else
+    k_generate_chain<N, NS, MODE, -1, false><<<g, HK_CHAIN_T, 0, st>>>(a);
 }
 
 template <int MODE, int N>
@@ -927,6 +946,33 @@ int hk_phsp_decay_chain(const double* d_w_in, const double* const* d_p4_in,
                                            : dispatch_chain<HK_RNG_PHILOX>(a, grid, st);
 }
 
+// When may the fused chain use the decaying daughter's mass m_k as its frame
+// mass instead of recomputing sqrt(E^2 - p^2) per event (phasespace.py:259-262)?
+// The daughter is generated with mass m_k, so the recomputed mass differs from
+// m_k only by the rounding of E^2 - p^2: relative error <= ~8 ulp * gamma^2
+// (E^2 and p^2 each carry a few ulp of E^2 = gamma^2 m^2).  Returns m_k (fast
+// path) when, over the whole phase space, that error is below 1e-14 (gamma <=
+// 4; boosted momenta then move by <~1e-14 * E, the parity budget being 1e-12 * E)
+// and m_k is within a quarter of the mismatch tolerance of the sub-decay
+// mother mass, so no event can fail the reference's per-event check; else 0
+// (the per-event path with the check).
+//   gamma bound: E_k <= (M^2 + m_k^2 - (sum of the other masses)^2) / (2M) in the
+//   mother frame; a moving mother multiplies gamma by at most 2 gamma_mother.
+double fixed_frame_mass(const hk_decay_t& d, int k, const hk_decay_t& sub) {
+  const double mk = d.masses[k], M = d.mother_mass;
+  if (!(mk > 0.0) || !std::isfinite(mk) || !(M > 0.0) || !std::isfinite(M)) return 0.0;
+  const double tol = 1e-9 * (sub.mother_mass > 1e-6 ? sub.mother_mass : 1e-6);
+  if (!(std::fabs(mk - sub.mother_mass) <= 0.25 * tol)) return 0.0;
+  double others = 0.0;
+  for (int j = 0; j < d.n; ++j)
+    if (j != k) others += d.masses[j];
+  const double e_max = (M * M + mk * mk - others * others) / (2.0 * M);
+  double gamma = e_max / mk;
+  if (d.moving) gamma *= 2.0 * (d.mother[0] / d.m_mother);  // NaN / inf fail the test below
+  if (!(gamma >= 1.0 - 1e-12) || !(gamma <= 4.0)) return 0.0;
+  return mk;
+}
+
 int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t daughter_index,
                            const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
                            int64_t ev_count, double* const* d_cols, double* d_wpartials,
@@ -958,6 +1004,8 @@ int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t 
   }
   a.wpart = d_wpartials;
   a.first_bad = reinterpret_cast<unsigned long long*>(d_first_bad);
+  a.fixed_m = fixed_frame_mass(*spec, a.k, *sub);
+  a.fixed_im = a.fixed_m > 0.0 ? 1.0 / a.fixed_m : 0.0;
   const unsigned grid = chunk_grid(num_chunks(ev_count));
   cudaStream_t st = as_stream(stream);
   return key->mode == HK_RNG_REFERENCE ? dispatch_gen_chain<HK_RNG_REFERENCE>(a, grid, st)

@@ -250,6 +250,17 @@ def test_chain_vs_golden(cuda, hk, golden):
     assert_block_parity(_arr(ch), arrays["chain_c3_window_5000"], 4, "window")
 
 
+def _fused_vs_two_step(fused, two, k: int, n_sub: int):
+    """The fused chain against generate + decay_chain: weights and every
+    parent-daughter column bit-identical; the sub-decay columns (the fixed-frame
+    boost path, hk_phsp_generate_chain) within the parity budget |dc| <= 1e-12 E."""
+    sub_rows = set(range(1 + 4 * (k - 1), 1 + 4 * (k - 1 + n_sub)))
+    for r in range(fused.shape[0]):
+        if r not in sub_rows:
+            assert np.array_equal(fused[r], two[r], equal_nan=True), f"column {r} differs"
+    assert_block_parity(fused, two, fused.shape[0] // 4, "fused vs two-step")
+
+
 def test_fused_chain_equals_two_step(cuda, hk, oracle):
     spec, mother = _b0(hk)
     sub = hk.DecaySpec(M_JPSI, (M_MU, M_MU))
@@ -258,11 +269,14 @@ def test_fused_chain_equals_two_step(cuda, hk, oracle):
                                    hk.RngKey(2, 1)))
     fused = hk.phsp_generate_chain(spec, mother, n, hk.RngKey(1, 1), 1, sub, hk.RngKey(2, 1))
     assert fused.schema.names == hk.phsp_schema(4).names
-    assert np.array_equal(_arr(fused), two, equal_nan=True)
+    _fused_vs_two_step(_arr(fused), two, 1, 2)
     ref = oracle.decay_chain(oracle.generate(B0_DAUGHTERS, B0_MASS, n, 1, 1, threads=8), 1,
                              (M_MU, M_MU), M_JPSI, 2, 1, threads=8)
     assert_block_parity(two, np.stack(list(ref.values())), 4, "C3")
-    # sub-decay on daughter 3 (pion -> two photons-like massless pair)
+    assert_block_parity(_arr(fused), np.stack(list(ref.values())), 4, "C3 fused")
+    # sub-decay on daughter 3 (pion -> two photons-like massless pair): gamma
+    # up to ~16 fails the fixed-frame bound, so this runs the per-event frame
+    # mass path, bit-identical to the two-step chain
     sub3 = hk.DecaySpec(B0_DAUGHTERS[2], (0.0, 0.0))
     a = _arr(hk.phsp_generate_chain(spec, mother, 5000, hk.RngKey(5, 1), 3, sub3, hk.RngKey(6, 1)))
     b = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, mother, 5000, hk.RngKey(5, 1)), 3, sub3,
@@ -272,8 +286,9 @@ def test_fused_chain_equals_two_step(cuda, hk, oracle):
 
 def test_fused_chain_moving_mother_and_ragged(cuda, hk, oracle):
     """The fused chain with a boosted parent (the generator's non-ILP boost
-    path) and a ragged size: bit-identical to generate + decay_chain, and
-    within the parity budget of the oracle's generate + decay_chain."""
+    path) and a ragged size: against generate + decay_chain (parent columns
+    and weights bit-identical) and within the parity budget of the oracle's
+    generate + decay_chain."""
     spec = hk.DecaySpec(B0_MASS, B0_DAUGHTERS)
     p = (0.7, -1.9, 3.3)
     e = math.sqrt(B0_MASS ** 2 + sum(c * c for c in p))
@@ -283,13 +298,39 @@ def test_fused_chain_moving_mother_and_ragged(cuda, hk, oracle):
     fused = _arr(hk.phsp_generate_chain(spec, mother, n, hk.RngKey(8, 1), 1, sub, hk.RngKey(9, 1)))
     two = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, mother, n, hk.RngKey(8, 1)), 1, sub,
                                    hk.RngKey(9, 1)))
-    assert np.array_equal(fused, two, equal_nan=True)
+    _fused_vs_two_step(fused, two, 1, 2)
     par = oracle.generate(B0_DAUGHTERS, B0_MASS, n, 8, 1, mother=(e, *p), threads=4)
     ref = oracle.decay_chain(par, 1, (M_MU, M_MU), M_JPSI, 9, 1, threads=4)
     assert_block_parity(fused, np.stack(list(ref.values())), 4, "moving-mother chain")
     tot = [sum(fused[1 + 4 * k + c] for k in range(4)) for c in range(4)]
     for got, want in zip(tot, (e, *p)):
         assert np.max(np.abs(got - want)) <= 1e-9 * e
+
+
+def test_fused_chain_fixed_frame_paths(cuda, hk, oracle):
+    """The fixed-frame fused chain (frame mass = m_k, host-proved) with a
+    three-body sub-decay (boost_m per daughter) against the two-step chain and
+    the oracle; a sub-decay whose mother mass is off by 0.5 of the mismatch
+    tolerance takes the per-event path (bit-identical to two-step, no error);
+    one off by 2x the tolerance raises the reference's error at event 0."""
+    spec, mother = _b0(hk)
+    n = 3 * 4096 + 77
+    sub = hk.DecaySpec(M_JPSI, (M_MU, M_MU, 0.0))
+    fused = _arr(hk.phsp_generate_chain(spec, mother, n, hk.RngKey(3, 1), 1, sub, hk.RngKey(4, 1)))
+    two = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, mother, n, hk.RngKey(3, 1)), 1, sub,
+                                   hk.RngKey(4, 1)))
+    _fused_vs_two_step(fused, two, 1, 3)
+    ref = oracle.decay_chain(oracle.generate(B0_DAUGHTERS, B0_MASS, n, 3, 1, threads=4), 1,
+                             (M_MU, M_MU, 0.0), M_JPSI, 4, 1, threads=4)
+    assert_block_parity(fused, np.stack(list(ref.values())), 5, "fixed-frame 3-body sub")
+    near = hk.DecaySpec(M_JPSI * (1 + 0.5e-9), (M_MU, M_MU))
+    a = _arr(hk.phsp_generate_chain(spec, mother, 5000, hk.RngKey(3, 1), 1, near, hk.RngKey(4, 1)))
+    b = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, mother, 5000, hk.RngKey(3, 1)), 1, near,
+                                 hk.RngKey(4, 1)))
+    assert np.array_equal(a, b, equal_nan=True)
+    far = hk.DecaySpec(M_JPSI * (1 + 2e-9), (M_MU, M_MU))
+    with pytest.raises(ValueError, match=r"event 0: daughter 1 mass .* does not match"):
+        hk.phsp_generate_chain(spec, mother, 5000, hk.RngKey(3, 1), 1, far, hk.RngKey(4, 1))
 
 
 def test_chain_mass_mismatch_names_event(cuda, hk):
