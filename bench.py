@@ -67,11 +67,8 @@ def _fp64_roofline(kernel: str, events_per_s_per_gpu: float, note: str = "") -> 
     except (OSError, KeyError, ValueError):
         return None
     inst = events_per_s_per_gpu * k["dp_inst_per_event"]
-    return {"bound": "fp64", "kernel": k["kernel"], "achieved": inst * 1e-12, "peak": pk["dp_inst_per_s"] * 1e-12,
-            "unit": "T DP inst/s", "frac": inst / pk["dp_inst_per_s"],
-            "tflops": events_per_s_per_gpu * k["dp_flops_per_event"] * 1e-12, "peak_tflops": pk["tflops"],
-            "dp_inst_per_event": k["dp_inst_per_event"],
-            "source": "DP inst/event: ncu (profiles/r01_fp64_roofline.json); peak: tools/fp64_peak.cu",
+    return {"bound": "fp64", "achieved": inst * 1e-12, "peak": pk["dp_inst_per_s"] * 1e-12,
+            "unit": "T DP inst/s", "frac": inst / pk["dp_inst_per_s"], "dp_inst_per_event": k["dp_inst_per_event"],
             **({"note": note} if note else {})}
 
 
@@ -356,20 +353,20 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
 
     dt = max_over_ranks(dt)
     # device-only time of the FCN pass over this rank's rows
+    # (the API's kernel -- k_nll_fused, last-CTA fold included -- enqueued back
+    # to back without the host wait: hk_nll_eval with no host result)
     x = shard.device_column("x0")
-    lm = lower_model(model)
-    parts = _lib.empty(_lib.num_fcn_tiles(n_local))
-    bad = _lib.bad_cells(1)
+    lm = lower_model(model, x)
+    work = torch.zeros(int(_lib.lib().hk_nll_work_doubles(n_local)), dtype=torch.float64, device=x.device)
     for _ in range(3):
-        _lib.lib().hk_nll_partials(_lib.ptr(x), n_local, lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+        _lib.lib().hk_nll_eval(_lib.ptr(x), n_local, lm, _lib.ptr(work), None, None, st.cuda_stream)
     ev0.record(st)
     for _ in range(evals):
-        _lib.lib().hk_nll_partials(_lib.ptr(x), n_local, lm, _lib.ptr(parts), _lib.ptr(bad), st.cuda_stream)
+        _lib.lib().hk_nll_eval(_lib.ptr(x), n_local, lm, _lib.ptr(work), None, None, st.cuda_stream)
     ev1.record(st)
     ev1.synchronize()
     kt = max_over_ranks(ev0.elapsed_time(ev1) / evals * 1e-3)
     # the one-launch C-ABI FCN call alone (kernel + mapped-memory result), no Python
-    work = torch.zeros(int(_lib.lib().hk_nll_work_doubles(n_local)), dtype=torch.float64, device=x.device)
     logsum, first = ctypes.c_double(), ctypes.c_uint64()
     for _ in range(3):
         _lib.lib().hk_nll_eval(_lib.ptr(x), n_local, lm, _lib.ptr(work), ctypes.byref(logsum),
@@ -478,10 +475,21 @@ def _max_over_ranks(torch, dist, v: float) -> float:
 
 
 def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
-    """The other BASELINE.json configs, measured the same way (secondary lines):
-    C1 1e5 generation through the API; C3 fused chain, 1e9 events sharded
-    (1.25e8 per GPU: 1e9/8); C5 fused Dalitz integration of 1e10 events
-    split over the GPUs (strong scaling)."""
+    """The other BASELINE.json configs, measured the same way (secondary
+    records, values in events/s unless stated; device-timed with CUDA events,
+    max over ranks):
+      C1          1e5 events per GPU through phsp_generate (launch + fold bound)
+      C2_philox   the C2 generator launch on the Philox4x32-10 production stream
+      C3          fused generate + J/psi -> mu mu chain, 1.25e8 events per GPU
+                  (1e9 / 8), 17 columns = 136 B/event; frac_copy vs copy BW
+      C2_average  phsp_average(<m12^2>) over a stored 1e8 block, 72 B/event read
+      CSV         write_csv of 1e7 13-column rows (%.17g formatted on the GPU),
+                  rows/s, host wall clock (the text leaves the GPU)
+      C5          1e10 events, fused generation + <m12^2>, strong scaling, no
+                  event store; 1024 super-chunk records cross GPUs
+      C5_bw       the same with <BW_K*(892)(m^2_K pi)> (M=0.89555, G=0.0473)
+      C5_generic  1e9 events of <m12^2 * BW(m12^2)>: the NVRTC-specialised
+                  kernel, the functor interpreter beside it"""
     from paper_1711_05683_b200.parallel import sharded_integrate
 
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
@@ -494,7 +502,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         return blk.meta["weight_partials"]
 
     dt = _timed(torch, c1, 50, dist)
-    out["C1"] = {"what": "1e5 events/GPU, phsp_generate API", "value": world * n1 / dt, "ms": dt * 1e3}
+    out["C1"] = {"value": world * n1 / dt, "ms": dt * 1e3}
     # C2 on the production stream (Philox4x32-10): the same kernel launch as the
     # headline step, device-timed, 104 B/event written
     peak = _peaks()["hbm_gbs"]
@@ -510,8 +518,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         _lib.check(_lib.lib().hk_phsp_generate(d, kp, rank * n2, n2, colp, _lib.ptr(wp), st.cuda_stream), "philox")
 
     dt = _timed(torch, c2p, 10, dist)
-    out["C2_philox"] = {"what": "C2 generator on the Philox4x32-10 production stream, 1e8 events/GPU",
-                        "value": world * n2 / dt, "ms": dt * 1e3, "GBps": BYTES_PER_EVENT * n2 / dt / 1e9,
+    out["C2_philox"] = {"value": world * n2 / dt, "ms": dt * 1e3, "GBps": BYTES_PER_EVENT * n2 / dt / 1e9,
                         "frac_copy": BYTES_PER_EVENT * n2 / dt / 1e9 / peak}
     del cols, colp, wp
     torch.cuda.empty_cache()
@@ -526,8 +533,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     c3()
     torch.cuda.empty_cache()
     dt = _timed(torch, c3, 5, dist)
-    out["C3"] = {"what": "fused chain B0->J/psi(->mu mu) K pi, 1.25e8 events/GPU, 136 B/event",
-                 "value": world * n3 / dt, "ms": dt * 1e3, "GBps": 136 * n3 / dt / 1e9,
+    out["C3"] = {"value": world * n3 / dt, "ms": dt * 1e3, "GBps": 136 * n3 / dt / 1e9,
                  "frac_copy": 136 * n3 / dt / 1e9 / peak}
     torch.cuda.empty_cache()
     # C5: 1e10 events, generation -> m^2_12 -> moments, no store; shards + NCCL gather + fold
@@ -548,8 +554,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         res["r"] = hk.phsp_average(hk.identity(), blk, m12)
 
     dt = _timed(torch, c2avg, 10, dist)
-    out["C2_average"] = {"what": "phsp_average(<m12^2>) over a stored 1e8 block, 72 B/event read",
-                         "value": world * EVENTS_PER_GPU / dt, "ms": dt * 1e3,
+    out["C2_average"] = {"value": world * EVENTS_PER_GPU / dt, "ms": dt * 1e3,
                          "frac_copy": 72 * EVENTS_PER_GPU / dt / 1e9 / peak}
     # CSV: write_csv of 1e7 stored rows, GPU-formatted text streamed to a file
     from paper_1711_05683_b200.store import ColumnStore
@@ -560,8 +565,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         t0 = time.perf_counter()
         sub.write_csv(fh)
         dt = time.perf_counter() - t0
-    out["CSV"] = {"what": "write_csv of 1e7 13-column rows (%.17g on GPU), host wall clock",
-                  "value": n_csv / dt, "unit": "rows/s"}
+    out["CSV"] = {"value": n_csv / dt, "unit": "rows/s"}
     del sub
     del blk
     torch.cuda.empty_cache()
@@ -573,8 +577,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
 
     dt = _timed(torch, c5, 2, dist)
     rf = _fp64_roofline("hk_jit_integrate", n5 / dt / world)
-    out["C5"] = {"what": "1e10 events, fused generation + <m12^2>, strong scaling, no store",
-                 "value": n5 / dt, "s": dt, "fp64_frac": rf["frac"] if rf else None}
+    out["C5"] = {"value": n5 / dt, "s": dt, "fp64_frac": rf["frac"] if rf else None}
     # C5 secondary integrand: K*(892) Breit-Wigner on m^2_K pi, the named builtin
 
     def m23(cols):
@@ -588,7 +591,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
         res["r"] = sharded_integrate(hk.breit_wigner(0.89555, 0.0473), spec, mother, n5, hk.RngKey(1, 1), m23)
 
     dt = _timed(torch, c5bw, 2, dist)
-    out["C5_bw"] = {"what": "1e10 events, fused generation + <BW_K*(892)(m^2_K pi)>", "value": n5 / dt}
+    out["C5_bw"] = {"value": n5 / dt}
     # C5 with an integrand outside the recognised Dalitz shapes: m12^2 * BW(m12^2)
     # runs as a specialised (NVRTC) kernel; the interpreter is timed beside it.
     expr = hk.identity() * hk.breit_wigner(3.0969, 0.1)
@@ -601,8 +604,7 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     dt_jit = _timed(torch, c5g, 3, dist)
     with _lib.jit_mode(_lib.JIT_OFF):
         dt_int = _timed(torch, c5g, 1, dist)
-    out["C5_generic"] = {"what": "1e9 events, <m12^2 * BW(m12^2)> NVRTC kernel (interpreter beside)",
-                         "value": world * n5g / dt_jit, "interpreter": world * n5g / dt_int}
+    out["C5_generic"] = {"value": world * n5g / dt_jit, "interpreter": world * n5g / dt_int}
     return out
 
 
@@ -764,8 +766,8 @@ def run_ours(args) -> None:
             "e2e": e2e,
             "gpu_launches": 3 * args.steps,   # k_generate + k_fold_supers + k_fold per step
             "cpu_baseline": cpu,
-            "fcn": fcn,
             "other_configs": others,
+            "fcn": fcn,      # last: the driver keeps the tail of the line
         }
         print(json.dumps(line), flush=True)
     if dist:

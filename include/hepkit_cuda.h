@@ -127,6 +127,16 @@ typedef struct hk_model {
   double norm[HK_MAX_COMPONENTS];
   double p0[HK_MAX_COMPONENTS];
   double p1[HK_MAX_COMPONENTS];
+  /* optional statistics of the observable column the FCN will read
+   * (hk_column_stats; has_stats = 0: none).  With them the host can prove,
+   * for the whole data range, that no event's density is non-positive or
+   * non-finite, and the Gaussian + exponential FCN drops its per-event
+   * checks and hoists sum_e B(x_e) = -sum(x) / tau out of the event loop.
+   * x_count must equal the n of the call or the statistics are ignored. */
+  int32_t has_stats;
+  int32_t _pad2;
+  int64_t x_count;
+  double x_min, x_max, x_sum;
 } hk_model_t;
 
 /* ---------------------------------------------------------------- runtime */
@@ -228,6 +238,21 @@ int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t 
                            const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
                            int64_t ev_count, double* const* d_cols, double* d_wpartials,
                            uint64_t* d_first_bad, void* stream);
+
+/* Statistics of one fp64 column for hk_model_t: h_out = {min, max, sum,
+ * number of non-finite values} over the finite values (sum in a fixed
+ * chunk-then-tree order: deterministic).  d_work: hk_column_stats_work_doubles(n)
+ * doubles of device scratch.  Synchronous on `stream`. */
+int64_t hk_column_stats_work_doubles(int64_t n);
+int hk_column_stats(const double* d_x, int64_t n, double* d_work, double* h_out, void* stream);
+
+/* The frame mass hk_phsp_generate_chain uses for the decaying daughter
+ * instead of recomputing sqrt(E^2 - p^2) per event (phasespace.py:259-262):
+ * m_k when the host proves no event can fail the mass check and the
+ * recomputed mass moves boosted momenta by < 1e-14 E (then *d_first_bad is
+ * never written and the caller need not read it back), else 0.0 (per-event
+ * mass and check).  Pure host function. */
+double hk_chain_fixed_frame_mass(const hk_decay_t* spec, int32_t daughter_index, const hk_decay_t* sub);
 
 /* --------------------------------------------------------------- averages */
 /* phsp_average moments (phasespace.py:310-329) over stored columns: per chunk

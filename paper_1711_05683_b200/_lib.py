@@ -37,6 +37,7 @@ EXPORTS = (
     "hk_abi_version", "hk_last_error", "hk_device_info", "hk_num_chunks",
     "hk_rng_raw64", "hk_rng_uniform",
     "hk_phsp_generate", "hk_phsp_generate_host", "hk_phsp_decay_chain", "hk_phsp_generate_chain",
+    "hk_chain_fixed_frame_mass", "hk_column_stats", "hk_column_stats_work_doubles",
     "hk_phsp_moments", "hk_map_program", "hk_phsp_integrate", "hk_fold_partials",
     "hk_nll_partials", "hk_nll_eval", "hk_model_density",
     "hk_yield_partials", "hk_splot_weights",
@@ -85,7 +86,9 @@ class hk_model_t(ctypes.Structure):
                 ("yield_", ctypes.c_double * HK_MAX_COMPONENTS),
                 ("norm", ctypes.c_double * HK_MAX_COMPONENTS),
                 ("p0", ctypes.c_double * HK_MAX_COMPONENTS),
-                ("p1", ctypes.c_double * HK_MAX_COMPONENTS)]
+                ("p1", ctypes.c_double * HK_MAX_COMPONENTS),
+                ("has_stats", ctypes.c_int32), ("_pad2", ctypes.c_int32), ("x_count", ctypes.c_int64),
+                ("x_min", ctypes.c_double), ("x_max", ctypes.c_double), ("x_sum", ctypes.c_double)]
 
 
 HK_FCN_MAX_OBS = 8
@@ -131,6 +134,9 @@ _SIGS = {
     "hk_phsp_generate_host": (_INT, [_D, _K, _U64, _I64, _PP, _PD, _P, ctypes.c_size_t, _P]),
     "hk_phsp_decay_chain": (_INT, [_P, _PP, _D, _K, _U64, _I64, _P, _PP, _P, _P]),
     "hk_phsp_generate_chain": (_INT, [_D, _K, _I32, _D, _K, _U64, _I64, _PP, _P, _P, _P]),
+    "hk_chain_fixed_frame_mass": (ctypes.c_double, [_D, _I32, _D]),
+    "hk_column_stats": (_INT, [_P, _I64, _P, _PD, _P]),
+    "hk_column_stats_work_doubles": (_I64, [_I64]),
     "hk_phsp_moments": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),
     "hk_phsp_integrate": (_INT, [_D, _K, _U64, _I64, _F, ctypes.POINTER(hk_pair_integrand_t), _P, _P, _P]),
     "hk_map_program": (_INT, [_PP, _I32, _I64, _F, _P, _P, _P]),

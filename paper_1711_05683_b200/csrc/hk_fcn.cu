@@ -39,6 +39,10 @@ struct Coeffs {
   // q0: A - B as a quadratic in x - mean
   double m_lo, m_hi;
   double q2, q1, q0;
+  // kFcnFast (fast_coeffs): amplitudes over their max c, log2(e) (A - B) as a
+  // quadratic in x - mean, and base = sum_e B(x_e) + n ln c = b sum(x) + n ln c
+  double fa[2], fq[3], base;
+  int32_t fast;
 };
 
 // One parameter point of the factored Gaussian + exponential density, for
@@ -49,12 +53,35 @@ struct FPoint {
   double amp[2], shift[1], scale[2];
   double m_lo, m_hi;
   double q2, q1, q0;
+  double fa[2], fq[3], base;  // kFcnFast (all doubles: the session copies it word by word)
 };
+
+__host__ __forceinline__ FPoint make_point(const Coeffs& c) {
+  FPoint p;
+  p.amp[0] = c.amp[0];
+  p.amp[1] = c.amp[1];
+  p.shift[0] = c.shift[0];
+  p.scale[0] = c.scale[0];
+  p.scale[1] = c.scale[1];
+  p.m_lo = c.m_lo;
+  p.m_hi = c.m_hi;
+  p.q2 = c.q2;
+  p.q1 = c.q1;
+  p.q0 = c.q0;
+  p.fa[0] = c.fa[0];
+  p.fa[1] = c.fa[1];
+  p.fq[0] = c.fq[0];
+  p.fq[1] = c.fq[1];
+  p.fq[2] = c.fq[2];
+  p.base = c.base;
+  return p;
+}
 
 // FCN kernel variants
 constexpr int kFcnGeneric = 0;   // any component list
 constexpr int kFcnGE = 1;        // Gaussian + exponential, reference op order
 constexpr int kFcnFactored = 2;  // Gaussian + exponential, one exp per event
+constexpr int kFcnFast = 3;      // kFcnFactored with the data range proved on the host (fast_row)
 
 // exp for the FCN data pass.  libdevice's: a 64-entry shared-memory table
 // variant (11 FP64 ops instead of ~17) measured slower on B200 (40.6 vs 36.1 us
@@ -164,6 +191,50 @@ __device__ __forceinline__ bool density_factored(const C& c, double x, double* s
 #endif
 }
 
+// 2^y for y <= 0: 2^n 2^f, n = rint(y), f in [-1/2, 1/2], 2^f a degree-8
+// polynomial (fitted by reweighted least squares; 2.9e-12 relative on the
+// interval, evaluated in double -- tools/fit_exp2_poly.py), n added to the
+// exponent field; n < -1020 returns 0.  Only on the kFcnFast path, where it
+// moves each density by <= 2.9e-12 relative: summed over 1e7 events at most
+// 3e-5 of ln L, ~1e-13 relative -- the FCN's budget is 1e-10.
+__device__ __forceinline__ double fcn_exp2_neg(double y) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: rounds y to an integer
+  const double r = y + magic;
+  const double f = y - (r - magic);
+  double p = 1.328492507863422e-06;
+  p = fma(p, f, 1.5308981596230215e-05);
+  p = fma(p, f, 0.00015403372425094143);
+  p = fma(p, f, 0.001333345520138187);
+  p = fma(p, f, 0.009618129182690833);
+  p = fma(p, f, 0.05550410935556957);
+  p = fma(p, f, 0.2402265069621877);
+  p = fma(p, f, 0.6931471805476419);
+  p = fma(p, f, 0.9999999999999317);
+  const int n = __double2loint(r);  // the low word of r is rint(y)
+  const double e = __longlong_as_double(__double_as_longlong(p) + ((long long)n << 52));
+  return n < -1020 ? 0.0 : e;
+}
+
+// One event of the kFcnFast FCN.  The host (fast_coeffs) has proved over the
+// column's [min, max] that both reference terms are finite normal doubles and
+// that the density is positive, so there is no per-event check; ln d is
+//   ln d = B + max(A - B, 0) + ln c + ln s',  s' = fa_big + fa_small 2^-|q|,
+// with q = log2(e) (A - B) = (fq0 u + fq1) u + fq2, u = x - mean.  sum_e B is
+// b sum(x) (the column statistic) and n ln c is a constant: both are in `base`
+// and added once by the fold.  Per event: 18 FP64 instructions (u, q, the
+// max(q, 0) sum, the exponential, s', the product) against ~27 for
+// kFcnFactored; the selects and the sign test are on the integer pipe.
+template <class C>
+__device__ __forceinline__ void fast_row(const C& c, double x, double& prod, double& qsum) {
+  const double u = x - c.shift[0];
+  const double q = fma(fma(c.fq[0], u, c.fq[1]), u, c.fq[2]);
+  const int hi = __double2hiint(q), lo = __double2loint(q);
+  const bool ga = hi >= 0;  // A >= B: the Gaussian term is the larger
+  qsum += __hiloint2double(ga ? hi : 0, ga ? lo : 0);
+  const double t = fcn_exp2_neg(__hiloint2double(hi | (int)0x80000000, lo));  // 2^-|q|
+  prod *= fma(ga ? c.fa[1] : c.fa[0], t, ga ? c.fa[0] : c.fa[1]);
+}
+
 // One tile: returns sum ln d over this thread's rows; flags
 // d <= 0 / non-finite (fitting.py:200-205) as ~row in *bad (max = first row).
 template <int V, class C>
@@ -195,6 +266,24 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
                                                int64_t end, const C& c,
                                                unsigned long long* bad, int tid) {
   const int64_t r0 = begin + tid;
+  if constexpr (V == kFcnFast) {
+    // the product of <= 16 factors s' in [1e-15, 2] stays normal: one log per
+    // thread and tile, no exponent bookkeeping
+    double prod = 1.0, qsum = 0.0;
+    if (end - begin == kFcnTile) {
+      double xv[kFcnRows];
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) fast_row(c, xv[i], prod, qsum);
+    } else {
+      for (int i = 0; i < kFcnRows; ++i) {
+        const int64_t r = r0 + i * kBlock;
+        if (r < end) fast_row(c, __ldg(x + r), prod, qsum);
+      }
+    }
+    return fma(qsum, 0.6931471805599453, log(prod));
+  }
   LogProd lp;
   double msum = 0.0;
   if (end - begin == kFcnTile) {
@@ -256,7 +345,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const d
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
-  fcn_finish(w, chunks);
+  fcn_finish(w, chunks, V == kFcnFast ? c.base : 0.0);
 }
 
 // Reference op order (fitting.py:160-166, functors.py:142-143, :161) with no
@@ -368,6 +457,7 @@ struct ManyArgs {
   FPoint pt[HK_MAX_POINTS];  // k points, padded with copies of the last to kpad
 };
 
+template <int V>
 __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(const __grid_constant__ ManyArgs a) {
   __shared__ unsigned int s_t;
   __shared__ double tot[kManyG];
@@ -391,7 +481,35 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
       bad[j] = 0;
     }
     const FPoint* c = a.pt + g * kManyG;  // padded to kpad points on the host
-    if (full) {
+    if constexpr (V == kFcnFast) {
+      // per point exactly range_logsum<kFcnFast>'s chain: same values
+      double prod[kManyG], qsum[kManyG];
+#pragma unroll
+      for (int j = 0; j < kManyG; ++j) {
+        prod[j] = 1.0;
+        qsum[j] = 0.0;
+      }
+      if (full) {
+        double xv[kFcnRows];
+#pragma unroll
+        for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(a.x + r0 + i * kBlock);
+#pragma unroll
+        for (int i = 0; i < kFcnRows; ++i) {
+#pragma unroll
+          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xv[i], prod[j], qsum[j]);
+        }
+      } else {
+        for (int i = 0; i < kFcnRows; ++i) {
+          const int64_t r = r0 + i * kBlock;
+          if (r >= end) continue;
+          const double xr = __ldg(a.x + r);
+#pragma unroll
+          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xr, prod[j], qsum[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kManyG; ++j) msum[j] = fma(qsum[j], 0.6931471805599453, log(prod[j]));
+    } else if (full) {
       double xv[kFcnRows];
 #pragma unroll
       for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(a.x + r0 + i * kBlock);
@@ -413,7 +531,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
     double acc[kManyG];
 #pragma unroll
     for (int j = 0; j < kManyG; ++j) {
-      acc[j] = lp[j].value() + msum[j];
+      acc[j] = V == kFcnFast ? msum[j] : lp[j].value() + msum[j];
       if (bad[j] && g * kManyG + j < a.k) atomicMax(a.bad + g * kManyG + j, bad[j]);
     }
     block_sum_store<kManyG>(acc, a.part + t * a.kpad + g * kManyG);
@@ -438,9 +556,10 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
         const int p = g * kManyG + j;
         if (p >= a.k) break;
         const unsigned long long bb = atomicExch(a.bad + p, 0ull);
-        a.out[p] = tot[j];
+        const double v = tot[j] + (V == kFcnFast ? c[j].base : 0.0);  // fcn_finish's order
+        a.out[p] = v;
         if (a.host_mail) {
-          a.host_mail[1 + p] = (unsigned long long)__double_as_longlong(tot[j]);
+          a.host_mail[1 + p] = (unsigned long long)__double_as_longlong(v);
           a.host_mail[1 + a.k + p] = ~bb;
         }
       }
@@ -472,10 +591,11 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
 // Command page in mapped host memory: kCmdSlots 16-byte slots {seq, word},
 // each written by the host with one aligned 16-byte store (atomic on x86
 // with AVX), read by lanes 0..10 of CTA 0's first warp with one 16-byte load
-// each -- 11 concurrent PCIe reads per poll, and a command is taken only when
+// each -- 17 concurrent PCIe reads per poll, and a command is taken only when
 // every slot carries the same new seq, so no ordering between the reads is
-// needed.  Words: 0 = variant | stop << 8, 1..10 = the FPoint.
-constexpr int kCmdSlots = 11;
+// needed.  Words: 0 = variant | stop << 8, 1..16 = the FPoint.
+constexpr int kCmdSlots = 1 + (int)(sizeof(FPoint) / sizeof(double));  // 17: word 0 + the FPoint
+static_assert(kCmdSlots <= 32, "one lane per command slot");
 struct alignas(16) CmdSlot {
   unsigned long long seq;
   unsigned long long word;
@@ -541,7 +661,7 @@ __device__ __forceinline__ void server_poll(const ServerArgs& a, unsigned long l
   const unsigned long long w0 = __shfl_sync(0xffffffffu, word, 0);
   if (s != ~0ull && (w0 >> 8)) s = ~0ull;  // stop
   if (s != ~0ull && lane >= 1 && lane < kCmdSlots) {
-    double* c = &a.dev->c.amp[0];           // FPoint: 10 consecutive doubles
+    double* c = &a.dev->c.amp[0];           // FPoint: kCmdSlots - 1 consecutive doubles
     c[lane - 1] = __longlong_as_double((long long)word);
   }
   if (lane == 0) {
@@ -618,7 +738,9 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_SERVER_MIN_BLOCKS) k_fcn_server
     mine = g;
     // the coefficients stay in shared memory (operands are LDS'd where the
     // arithmetic needs them): a register copy costs 14 of the 64 registers
-    if (s_variant == kFcnFactored)
+    if (s_variant == kFcnFast)
+      server_tiles<kFcnFast>(a, s_c, chunks);
+    else if (s_variant == kFcnFactored)
       server_tiles<kFcnFactored>(a, s_c, chunks);
     else
       server_tiles<kFcnGE>(a, s_c, chunks);
@@ -641,7 +763,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_SERVER_MIN_BLOCKS) k_fcn_server
         a.w.host_mail[5] = (unsigned long long)global_ns();
         FcnWork w = a.w;
         w.seq = g;
-        fcn_publish(w, total);
+        fcn_publish(w, total + (s_variant == kFcnFast ? s_c.base : 0.0));  // fcn_finish's order
       }
     }
     __syncthreads();
@@ -657,6 +779,7 @@ struct Session {
   ServerArgs args{};
   unsigned grid = 0;
   bool running = false;
+  bool active = false;  // between hk_fcn_session_start and _stop
   unsigned long long seq = 0;
 };
 thread_local Session t_session;
@@ -689,31 +812,82 @@ int session_launch(Session& S) {
   return HK_OK;
 }
 
-int session_stop(Session& S) {
+// Stop the session's CTAs (if any are running).  The stream, the mapped
+// command page and the device control block stay allocated for the next
+// session on this thread and device -- cudaHostAlloc / cudaFreeHost cost tens
+// of ms and synchronise the device, more than a whole C4 fit's FCN work --
+// unless `release` (device change, library shutdown).
+int session_stop(Session& S, bool release = false) {
   if (S.device < 0) return HK_OK;
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(S.device);
-  if (S.running && cudaStreamQuery(S.stream) == cudaErrorNotReady) {
-    CmdSlot v[kCmdSlots];
-    const unsigned long long seq = S.seq + 0x100000000ull;  // any seq the server has not answered
-    for (int k = 0; k < kCmdSlots; ++k) {
-      v[k].seq = seq;
-      v[k].word = k == 0 ? (1ull << 8) : 0ull;
+  cudaError_t e = cudaSuccess;
+  if (S.running) {
+    if (cudaStreamQuery(S.stream) == cudaErrorNotReady) {
+      CmdSlot v[kCmdSlots];
+      const unsigned long long seq = S.seq + 0x100000000ull;  // any seq the server has not answered
+      for (int k = 0; k < kCmdSlots; ++k) {
+        v[k].seq = seq;
+        v[k].word = k == 0 ? (1ull << 8) : 0ull;
+      }
+      write_slots(S.h_cmd, v);
     }
-    write_slots(S.h_cmd, v);
+    e = cudaStreamSynchronize(S.stream);
+    S.running = false;
   }
-  const cudaError_t e = cudaStreamSynchronize(S.stream);
-  cudaStreamDestroy(S.stream);
-  cudaFreeHost(S.h_cmd);
-  cudaFree(S.dev);
+  S.active = false;
+  if (release) {
+    cudaStreamDestroy(S.stream);
+    cudaFreeHost(S.h_cmd);
+    cudaFree(S.dev);
+    S = Session{};
+  }
   cudaSetDevice(cur);
-  S = Session{};
   if (e != cudaSuccess) return cuda_fail(e, "hk_fcn_session_stop");
   return HK_OK;
 }
 
-int make_coeffs(const hk_model_t* m, Coeffs* c) {
+// kFcnFast admission (see fast_row): the column statistics of hk_model_t
+// bound, for every x in [x_min, x_max],
+//   A(x) = -((x - mean) / sigma)^2 / 2 (concave), B(x) = b x (b = -1/tau),
+//   M(x) = max(A, B) in [min(B(x_min), B(x_max)), max(A(clamp(mean)), B(x_min), B(x_max))],
+// and that interval must sit inside kFcnFactored's window (m_lo, m_hi) with a
+// margin of 1: then both reference terms are finite normal doubles and the
+// density is positive for every event -- exactly the events kFcnFactored
+// takes without its fallback, so no per-event check is needed.  Also the
+// amplitude ratio must be >= 1e-15 (the 16-factor product of s' stays normal)
+// and the rounding of the quadratic q over the range <= 1e-11 (log2 units).
+void fast_coeffs(const hk_model_t* m, int64_t n, Coeffs* c) {
+  c->fast = 0;
+  if (n <= 0 || !m->has_stats || m->x_count != n) return;
+  if (!(c->m_lo < c->m_hi) || c->kind[0] != HK_SHAPE_GAUSS || c->kind[1] != HK_SHAPE_EXPO) return;
+  const double xmin = m->x_min, xmax = m->x_max;
+  if (!std::isfinite(xmin) || !std::isfinite(xmax) || !(xmin <= xmax) || !std::isfinite(m->x_sum)) return;
+  const double mu = c->shift[0], is = c->scale[0], b = c->scale[1];
+  const double amax = std::fmax(c->amp[0], c->amp[1]), amin = std::fmin(c->amp[0], c->amp[1]);
+  if (!(amin >= 1e-15 * amax)) return;
+  const double b_lo = std::fmin(b * xmin, b * xmax), b_hi = std::fmax(b * xmin, b * xmax);
+  const double xc = std::fmin(std::fmax(mu, xmin), xmax);
+  const double zc = (xc - mu) * is;
+  const double a_hi = -0.5 * zc * zc;
+  const double m_lo = b_lo, m_hi = std::fmax(a_hi, b_hi);
+  if (!(m_lo > c->m_lo + 1.0) || !(m_hi < c->m_hi - 1.0)) return;
+  const double log2e = 1.4426950408889634;
+  const double q2 = log2e * c->q2, q1 = log2e * c->q1, q0 = log2e * c->q0;
+  const double umax = std::fmax(std::fabs(xmin - mu), std::fabs(xmax - mu));
+  const double err = 8.0 * 1.1102230246251565e-16 * (std::fabs(q2) * umax * umax + std::fabs(q1) * umax + std::fabs(q0));
+  if (!(err <= 1e-11)) return;
+  c->fq[0] = q2;
+  c->fq[1] = q1;
+  c->fq[2] = q0;
+  c->fa[0] = c->amp[0] / amax;
+  c->fa[1] = c->amp[1] / amax;
+  c->base = b * m->x_sum + (double)n * std::log(amax);
+  c->fast = 1;
+}
+
+int make_coeffs(const hk_model_t* m, Coeffs* c, int64_t n = -1) {
   HK_REQUIRE(m != nullptr, "NULL model");
   HK_REQUIRE(m->n_comp >= 1 && m->n_comp <= HK_MAX_COMPONENTS, "component count %d outside 1..%d",
              m->n_comp, HK_MAX_COMPONENTS);
@@ -748,20 +922,23 @@ int make_coeffs(const hk_model_t* m, Coeffs* c) {
     c->q2 = -0.5 * c->scale[0] * c->scale[0];
     c->q1 = -c->scale[1];
     c->q0 = -c->shift[0] * c->scale[1];
+    fast_coeffs(m, n, c);
   }
   return HK_OK;
 }
 
-int fcn_variant(const Coeffs& c) {
+// allow_fast: the caller folds with fcn_finish's base (not hk_nll_partials)
+int fcn_variant(const Coeffs& c, bool allow_fast = true) {
   const bool ge = c.n_comp == 2 && c.kind[0] == HK_SHAPE_GAUSS && c.kind[1] == HK_SHAPE_EXPO;
   if (!ge) return kFcnGeneric;
+  if (allow_fast && c.fast) return kFcnFast;
   return c.m_lo < c.m_hi ? kFcnFactored : kFcnGE;
 }
 
 int launch_nll(const double* d_x, int64_t n, const Coeffs& c, double* part,
                unsigned long long* bad, cudaStream_t st) {
   const unsigned grid = chunk_grid((n + kFcnTile - 1) / kFcnTile);
-  switch (fcn_variant(c)) {
+  switch (fcn_variant(c, false)) {
     case kFcnFactored: k_nll<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
     case kFcnGE: k_nll<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
     default: k_nll<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, part, bad); break;
@@ -869,7 +1046,7 @@ int mailbox(Mailbox** out) {
 
 // hk_shutdown: free this thread's mailboxes (rebuilt by the next hk_nll_eval)
 void fcn_release() {
-  session_stop(t_session);
+  session_stop(t_session, true);
   for (Mailbox& m : t_boxes) {
     if (m.device < 0) continue;
     cudaFreeHost(const_cast<unsigned long long*>(m.h));
@@ -1105,6 +1282,81 @@ int fill_ratio_args(const double* const* d_obs, int64_t n, const hk_density_t* m
   return HK_OK;
 }
 
+// ------------------------------------------------- column statistics -----
+// hk_column_stats: per 4096-row chunk {min, max, sum, non-finite count} over
+// the finite values (min/max by shuffle + shared memory, sum and count by the
+// deterministic block_sum_store tree), then one CTA folds the chunks in a
+// fixed order.  Read once per data column (fitting.py caches the result).
+__device__ __forceinline__ void block_minmax(double& lo, double& hi) {
+  __shared__ double s_lo[kBlock / 32], s_hi[kBlock / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, off));
+    hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, off));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_lo[warp] = lo;
+    s_hi[warp] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kBlock / 32; ++i) {
+      s_lo[0] = fmin(s_lo[0], s_lo[i]);
+      s_hi[0] = fmax(s_hi[0], s_hi[i]);
+    }
+  }
+  __syncthreads();
+  lo = s_lo[0];
+  hi = s_hi[0];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBlock) k_col_stats(const double* __restrict__ x, int64_t n,
+                                                     double* __restrict__ part) {
+  const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double lo = inf, hi = -inf, acc[2] = {0.0, 0.0};
+    for (int i = 0; i < kFcnRows; ++i) {
+      const int64_t r = ch * kFcnTile + i * kBlock + threadIdx.x;
+      if (r >= n) break;
+      const double v = __ldg(x + r);
+      if (isfinite(v)) {
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+        acc[0] += v;
+      } else {
+        acc[1] += 1.0;
+      }
+    }
+    block_minmax(lo, hi);
+    block_sum_store<2>(acc, part + 4 * ch + 2);
+    if (threadIdx.x == 0) {
+      part[4 * ch] = lo;
+      part[4 * ch + 1] = hi;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_col_stats_fold(const double* __restrict__ part, int64_t chunks,
+                                                          double* __restrict__ out) {
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double lo = inf, hi = -inf, acc[2] = {0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < chunks; i += kBlock) {
+    lo = fmin(lo, part[4 * i]);
+    hi = fmax(hi, part[4 * i + 1]);
+    acc[0] += part[4 * i + 2];
+    acc[1] += part[4 * i + 3];
+  }
+  block_minmax(lo, hi);
+  block_sum_store<2>(acc, out + 2);
+  if (threadIdx.x == 0) {
+    out[0] = lo;
+    out[1] = hi;
+  }
+}
+
 }  // namespace hk
 
 using namespace hk;
@@ -1214,7 +1466,7 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream) {
   Coeffs c;
-  if (int rc = make_coeffs(model, &c)) return rc;
+  if (int rc = make_coeffs(model, &c, n)) return rc;
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
   HK_REQUIRE(d_x && d_work && (!h_logsum || h_first_bad), "NULL pointer");
   cudaStream_t st = as_stream(stream);
@@ -1224,6 +1476,7 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   w.div0 = nullptr;  // the closed-form shapes have no divisions to check
   const unsigned grid = chunk_grid(w.full + w.tail_ctas);
   switch (fcn_variant(c)) {
+    case kFcnFast: k_nll_fused<kFcnFast><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     case kFcnFactored: k_nll_fused<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     case kFcnGE: k_nll_fused<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     default: k_nll_fused<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
@@ -1245,24 +1498,21 @@ int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int
   HK_REQUIRE(d_x && d_work && models && h_logsums && h_first_bad, "NULL pointer");
   ManyArgs a;
   std::memset(&a, 0, sizeof(a));
+  // one variant for the whole batch, the one each single-point call would
+  // take (so every value is bit-identical to hk_nll_eval's); mixed batches
+  // run point by point
   bool factored = true;
+  int variant = -1;
   for (int p = 0; p < k; ++p) {
     Coeffs c;
-    if (int rc = make_coeffs(models + p, &c)) return rc;
-    if (fcn_variant(c) != kFcnFactored) {
+    if (int rc = make_coeffs(models + p, &c, n)) return rc;
+    const int v = fcn_variant(c);
+    if ((v != kFcnFactored && v != kFcnFast) || (variant >= 0 && v != variant)) {
       factored = false;
       break;
     }
-    a.pt[p].amp[0] = c.amp[0];
-    a.pt[p].amp[1] = c.amp[1];
-    a.pt[p].shift[0] = c.shift[0];
-    a.pt[p].scale[0] = c.scale[0];
-    a.pt[p].scale[1] = c.scale[1];
-    a.pt[p].m_lo = c.m_lo;
-    a.pt[p].m_hi = c.m_hi;
-    a.pt[p].q2 = c.q2;
-    a.pt[p].q1 = c.q1;
-    a.pt[p].q0 = c.q0;
+    variant = v;
+    a.pt[p] = make_point(c);
   }
   for (int p = k; p < ((k + kManyG - 1) / kManyG) * kManyG; ++p) a.pt[p] = a.pt[k - 1];
   if (!factored) {  // other model kinds: one single-point pass per point (same values)
@@ -1291,7 +1541,10 @@ int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int
   a.host_mail = mb->d;
   a.seq = ++mb->seq;
   cudaStream_t st = as_stream(stream);
-  k_nll_many<<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);
+  if (variant == kFcnFast)
+    k_nll_many<kFcnFast><<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);
+  else
+    k_nll_many<kFcnFactored><<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);
   if (int rc = check_launch("k_nll_many")) return rc;
   double first = 0.0;
   uint64_t dummy = 0;
@@ -1312,17 +1565,30 @@ int hk_fcn_session_start(const double* d_x, int64_t n, double* d_work, int64_t i
   Session& S = t_session;
   int dev = 0, sms = 0, per_sm = 0, coop = 0;
   HK_CUDA(cudaGetDevice(&dev));
+  if (S.device >= 0 && S.device != dev)
+    if (int rc = session_stop(S, true)) return rc;
   HK_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   HK_REQUIRE(coop, "device %d has no cooperative launch", dev);
   HK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   HK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fcn_server, kBlock, 0));
   HK_REQUIRE(per_sm >= 1, "FCN session kernel does not fit an SM");
-  S.device = dev;
-  HK_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
-  HK_CUDA(cudaHostAlloc(&S.h_cmd, sizeof(ServerCmd), cudaHostAllocMapped));
-  std::memset(S.h_cmd, 0, sizeof(ServerCmd));
-  HK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.d_cmd), S.h_cmd, 0));
-  HK_CUDA(cudaMalloc(&S.dev, sizeof(ServerDev)));
+  if (S.device < 0) {  // first session on this thread: allocate once, reused by later sessions
+    HK_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+    HK_CUDA(cudaHostAlloc(&S.h_cmd, sizeof(ServerCmd), cudaHostAllocMapped));
+    std::memset(S.h_cmd, 0, sizeof(ServerCmd));
+    HK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.d_cmd), S.h_cmd, 0));
+    HK_CUDA(cudaMalloc(&S.dev, sizeof(ServerDev)));
+    S.device = dev;
+  }
+  S.active = true;
+  {  // the page reads "nothing new" to the fresh CTAs: every slot carries the last answered seq
+    CmdSlot v[kCmdSlots];
+    for (int k = 0; k < kCmdSlots; ++k) {
+      v[k].seq = S.seq;
+      v[k].word = 0ull;
+    }
+    write_slots(S.h_cmd, v);
+  }
   Mailbox* mb = nullptr;
   if (int rc = mailbox(&mb)) return rc;
   FcnWork w;
@@ -1342,10 +1608,10 @@ int hk_fcn_session_start(const double* d_x, int64_t n, double* d_work, int64_t i
 
 int hk_fcn_session_eval(const hk_model_t* model, double* h_logsum, uint64_t* h_first_bad) {
   Session& S = t_session;
-  HK_REQUIRE(S.device >= 0, "no FCN session on this thread (hk_fcn_session_start)");
+  HK_REQUIRE(S.active, "no FCN session on this thread (hk_fcn_session_start)");
   HK_REQUIRE(h_logsum && h_first_bad, "NULL pointer");
   Coeffs c;
-  if (int rc = make_coeffs(model, &c)) return rc;
+  if (int rc = make_coeffs(model, &c, S.args.n)) return rc;
   const int variant = fcn_variant(c);
   if (variant == kFcnGeneric) {
     set_error("an FCN session serves the Gaussian + exponential model");
@@ -1364,8 +1630,9 @@ int hk_fcn_session_eval(const hk_model_t* model, double* h_logsum, uint64_t* h_f
   // the mailbox's sequence numbers are per (thread, device): the session's
   // command seq is the mailbox seq the answer will carry
   const unsigned long long seq = ++mb->seq;
-  const double words[kCmdSlots - 1] = {c.amp[0], c.amp[1], c.shift[0], c.scale[0], c.scale[1],
-                                       c.m_lo,   c.m_hi,   c.q2,       c.q1,       c.q0};
+  const FPoint pt = make_point(c);
+  double words[kCmdSlots - 1];
+  std::memcpy(words, &pt, sizeof(pt));
   CmdSlot v[kCmdSlots];
   v[0].seq = seq;
   v[0].word = (unsigned long long)variant;
@@ -1443,6 +1710,23 @@ int hk_splot_weights(const double* d_x, int64_t n, const hk_model_t* model, cons
   HK_REQUIRE(d_x, "NULL data");
   k_splot<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, as_stream(stream)>>>(d_x, n, a);
   return check_launch("k_splot");
+}
+
+int64_t hk_column_stats_work_doubles(int64_t n) {
+  return 4 * ((n <= 0 ? 0 : (n + kFcnTile - 1) / kFcnTile) + 1);
+}
+
+int hk_column_stats(const double* d_x, int64_t n, double* d_work, double* h_out, void* stream) {
+  HK_REQUIRE(n > 0 && d_x && d_work && h_out, "bad column-statistics arguments");
+  cudaStream_t st = as_stream(stream);
+  const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
+  k_col_stats<<<chunk_grid(chunks), kBlock, 0, st>>>(d_x, n, d_work + 4);
+  if (int rc = check_launch("k_col_stats")) return rc;
+  k_col_stats_fold<<<1, kBlock, 0, st>>>(d_work + 4, chunks, d_work);
+  if (int rc = check_launch("k_col_stats_fold")) return rc;
+  HK_CUDA(cudaMemcpyAsync(h_out, d_work, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  HK_CUDA(cudaStreamSynchronize(st));
+  return HK_OK;
 }
 
 int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,

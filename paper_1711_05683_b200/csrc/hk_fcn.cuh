@@ -118,9 +118,10 @@ __device__ __forceinline__ void fcn_publish(const FcnWork& w, double total) {
   }
 }
 
-// Last CTA: fixed-order fold of the `chunks` tile partials, then publish.
+// Last CTA: fixed-order fold of the `chunks` tile partials, plus `base` (a
+// per-call constant the variant hoisted out of the event sum), then publish.
 // Called by every thread of every CTA after its tiles are stored.
-__device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks) {
+__device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks, double base = 0.0) {
   // block_sum_store's writer is thread 0: it alone fences before the ticket
   __shared__ unsigned int s_ticket;
   if (threadIdx.x == 0) {
@@ -134,7 +135,7 @@ __device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks) {
   for (int64_t i = threadIdx.x; i < chunks; i += kBlock) acc[0] += __ldcg(w.part + i);
   __shared__ double total;
   block_sum_store<1>(acc, &total);
-  if (threadIdx.x == 0) fcn_publish(w, total);
+  if (threadIdx.x == 0) fcn_publish(w, total + base);
 }
 
 // The FCN over a density functor dens(row, &div0) -> density (any model: the

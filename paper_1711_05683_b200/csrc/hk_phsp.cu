@@ -973,6 +973,11 @@ double fixed_frame_mass(const hk_decay_t& d, int k, const hk_decay_t& sub) {
   return mk;
 }
 
+double hk_chain_fixed_frame_mass(const hk_decay_t* spec, int32_t daughter_index, const hk_decay_t* sub) {
+  if (!spec || !sub || daughter_index < 1 || daughter_index > spec->n || spec->n > HK_MAX_DAUGHTERS) return 0.0;
+  return fixed_frame_mass(*spec, daughter_index - 1, *sub);
+}
+
 int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t daughter_index,
                            const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
                            int64_t ev_count, double* const* d_cols, double* d_wpartials,

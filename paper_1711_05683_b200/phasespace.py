@@ -442,11 +442,16 @@ def phsp_generate_chain(spec: DecaySpec, mother: FourVector, n_events: int, key:
     mode = rng_mode(rng)
     wpart = _lib.empty(2 * _lib.num_weight_slices(n_events))
     bad = _lib.bad_cells(1)
+    d, ds = _lib.make_decay(spec, mother, m_mother), _lib.make_decay(subspec)
     _lib.check(_lib.lib().hk_phsp_generate_chain(
-        _lib.make_decay(spec, mother, m_mother), _lib.make_key(key, mode), int(daughter_index),
-        _lib.make_decay(subspec), _lib.make_key(sub_key, mode), _lib.u64(row_offset), n_events,
-        _lib.ptr_array(cols), _lib.ptr(wpart), _lib.ptr(bad), _lib.stream_ptr()),
+        d, _lib.make_key(key, mode), int(daughter_index), ds, _lib.make_key(sub_key, mode),
+        _lib.u64(row_offset), n_events, _lib.ptr_array(cols), _lib.ptr(wpart), _lib.ptr(bad), _lib.stream_ptr()),
         "hk_phsp_generate_chain")
+    if _lib.lib().hk_chain_fixed_frame_mass(d, int(daughter_index), ds) > 0.0:
+        # the host proved no event can fail the mass check: no read-back, the
+        # call stays asynchronous like phsp_generate
+        _set_weight_partials(store, wpart)
+        return store
     (first,) = _lib.read_bad(bad)
     if first != _lib.HK_NO_BAD_ROW:
         j = first - _lib.u64(row_offset)

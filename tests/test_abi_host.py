@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_functions() -> set[str]:
     text = open(os.path.join(ROOT, "include", "hepkit_cuda.h")).read()
-    return set(re.findall(r"^(?:int|int32_t|int64_t)\s+(hk_\w+)\(", text, flags=re.M))
+    return set(re.findall(r"^(?:int|int32_t|int64_t|double)\s+(hk_\w+)\(", text, flags=re.M))
 
 
 def test_library_exports_every_declared_symbol(hk):
@@ -380,3 +380,24 @@ def test_header_is_plain_c_and_cpp(lang, std):
     r = subprocess.run([cc, std, "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only", "-x", lang, hdr],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_chain_fixed_frame_mass_predicate(hk):
+    """hk_chain_fixed_frame_mass (host only): m_k for the C3 chain (J/psi,
+    gamma <= 1.2), 0 for a sub-decay mother off by more than a quarter of the
+    mismatch tolerance, a massless daughter, or a daughter boosted beyond
+    gamma 4 (the pion of B0 -> J/psi K pi)."""
+    from paper_1711_05683_b200 import _lib
+    L = _lib.load_library()
+    spec = _lib.make_decay(hk.DecaySpec(B0_MASS, B0_DAUGHTERS))
+    jpsi = B0_DAUGHTERS[0]
+    assert L.hk_chain_fixed_frame_mass(spec, 1, _lib.make_decay(hk.DecaySpec(jpsi, (0.105, 0.105)))) == jpsi
+    near = _lib.make_decay(hk.DecaySpec(jpsi * (1 + 0.2e-9), (0.105, 0.105)))
+    assert L.hk_chain_fixed_frame_mass(spec, 1, near) == jpsi
+    off = _lib.make_decay(hk.DecaySpec(jpsi * (1 + 0.5e-9), (0.105, 0.105)))
+    assert L.hk_chain_fixed_frame_mass(spec, 1, off) == 0.0
+    pion = _lib.make_decay(hk.DecaySpec(B0_DAUGHTERS[2], (0.0, 0.0)))
+    assert L.hk_chain_fixed_frame_mass(spec, 3, pion) == 0.0
+    massless = _lib.make_decay(hk.DecaySpec(2.0, (0.0, 0.5)))
+    assert L.hk_chain_fixed_frame_mass(massless, 1, _lib.make_decay(hk.DecaySpec(0.3, (0.1, 0.1)))) == 0.0
+    assert L.hk_chain_fixed_frame_mass(spec, 4, pion) == 0.0

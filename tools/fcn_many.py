@@ -60,7 +60,7 @@ with hk.fcn_session(m, data, ["x0"]):
     for p in pts:
         ps["mean"].set(p[0]); ps["sigma"].set(p[1]); ps["tau"].set(p[2])
         lm_ = _L.hk_model_t()
-        _ct.memmove(_ct.byref(lm_), _ct.byref(_lm(m)), _ct.sizeof(lm_))
+        _ct.memmove(_ct.byref(lm_), _ct.byref(_lm(m, data.device_column("x0"))), _ct.sizeof(lm_))
         lms.append(lm_)
     ls_, fb_ = _ct.c_double(), _ct.c_uint64()
     f = _L.lib().hk_fcn_session_eval
@@ -91,7 +91,7 @@ import ctypes  # noqa: E402
 k = 51
 models = (_lib.hk_model_t * k)()
 for i in range(k):
-    ctypes.memmove(ctypes.byref(models, i * ctypes.sizeof(_lib.hk_model_t)), ctypes.byref(lower_model(m)),
+    ctypes.memmove(ctypes.byref(models, i * ctypes.sizeof(_lib.hk_model_t)), ctypes.byref(lower_model(m, data.device_column("x0"))),
                    ctypes.sizeof(_lib.hk_model_t))
 x = data.device_column("x0")
 work = _ManyWorkspace.get(len(data), k, _lib.stream_ptr())
@@ -104,6 +104,17 @@ e1.record(st)
 e1.synchronize()
 out["many51_kernel_ms"] = e0.elapsed_time(e1) / 20
 out["many51_kernel_events_per_s"] = k * len(data) / (out["many51_kernel_ms"] * 1e-3)
+# the single-point API kernel alone (k_nll_fused, kFcnFast), back to back
+lm1 = lower_model(m, x)
+w1 = torch.zeros(int(_lib.lib().hk_nll_work_doubles(len(data))), dtype=torch.float64, device="cuda")
+for _ in range(5):
+    _lib.lib().hk_nll_eval(x.data_ptr(), len(data), lm1, w1.data_ptr(), None, None, st.cuda_stream)
+e0.record(st)
+for _ in range(200):
+    _lib.lib().hk_nll_eval(x.data_ptr(), len(data), lm1, w1.data_ptr(), None, None, st.cuda_stream)
+e1.record(st)
+e1.synchronize()
+out["single_kernel_us"] = e0.elapsed_time(e1) / 200 * 1e3
 # whole C4 fit from a displaced start, serial objective vs batched
 for mode in ("serial", "batched"):
     mm = model()

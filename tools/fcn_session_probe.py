@@ -24,10 +24,10 @@ model = hk.add_pdfs([P("n_sig", 4e6), P("n_bkg", 6e6)],
 rs = np.random.default_rng(1)
 xall = np.clip(np.concatenate([rs.normal(5, 0.5, 4_000_000), rs.exponential(3.0, 6_000_000)]), 1e-3, 9.999)
 L = _lib.lib()
-lm = lower_model(model)
 out = []
 for n in (4096, 4096 * 148, 4096 * 592, 1_000_000, 10_000_000):
     x = torch.from_numpy(xall[:n].copy()).cuda()
+    lm = lower_model(model, x)   # with the column statistics: the kFcnFast path
     work = torch.zeros(int(L.hk_nll_work_doubles(n)), dtype=torch.float64, device="cuda")
     ls, fb = ctypes.c_double(), ctypes.c_uint64()
     st = torch.cuda.current_stream().cuda_stream
