@@ -191,49 +191,53 @@ __device__ __forceinline__ bool density_factored(const C& c, double x, double* s
 #endif
 }
 
-// 2^y for y <= 0: 2^n 2^f, n = rint(y), f in [-1/2, 1/2], 2^f a degree-8
-// polynomial (fitted by reweighted least squares; 2.9e-12 relative on the
-// interval, evaluated in double -- tools/fit_exp2_poly.py), n added to the
-// exponent field; n < -1020 returns 0.  Only on the kFcnFast path, where it
-// moves each density by <= 2.9e-12 relative: summed over 1e7 events at most
+// 2^f on f in [-1/2, 1/2]: degree-8 polynomial (fitted by reweighted least
+// squares; 2.9e-12 relative on the interval evaluated in double).  In the
+// constant bank so each DFMA takes its coefficient as an operand (no UMOV).
+__constant__ double kExp2Poly[9] = {1.328492507863422e-06,  1.5308981596230215e-05, 0.00015403372425094143,
+                                    0.001333345520138187,   0.009618129182690833,   0.05550410935556957,
+                                    0.2402265069621877,     0.6931471805476419,     0.9999999999999317};
+
+// 2^y for -1000 <= y <= 0 (the host proves the range, fast_coeffs): 2^n 2^f,
+// n = rint(y), f in [-1/2, 1/2], n added to the high word (2^f is normal and
+// 2^n >= 2^-1000, so the result is a normal double, no underflow path).
+// Moves each density by <= 2.9e-12 relative: summed over 1e7 events at most
 // 3e-5 of ln L, ~1e-13 relative -- the FCN's budget is 1e-10.
 __device__ __forceinline__ double fcn_exp2_neg(double y) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52: rounds y to an integer
   const double r = y + magic;
   const double f = y - (r - magic);
-  double p = 1.328492507863422e-06;
-  p = fma(p, f, 1.5308981596230215e-05);
-  p = fma(p, f, 0.00015403372425094143);
-  p = fma(p, f, 0.001333345520138187);
-  p = fma(p, f, 0.009618129182690833);
-  p = fma(p, f, 0.05550410935556957);
-  p = fma(p, f, 0.2402265069621877);
-  p = fma(p, f, 0.6931471805476419);
-  p = fma(p, f, 0.9999999999999317);
+  double p = kExp2Poly[0];
+#pragma unroll
+  for (int k = 1; k < 9; ++k) p = fma(p, f, kExp2Poly[k]);
   const int n = __double2loint(r);  // the low word of r is rint(y)
-  const double e = __longlong_as_double(__double_as_longlong(p) + ((long long)n << 52));
-  return n < -1020 ? 0.0 : e;
+  return __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
 }
 
 // One event of the kFcnFast FCN.  The host (fast_coeffs) has proved over the
 // column's [min, max] that both reference terms are finite normal doubles and
 // that the density is positive, so there is no per-event check; ln d is
 //   ln d = B + max(A - B, 0) + ln c + ln s',  s' = fa_big + fa_small 2^-|q|,
-// with q = log2(e) (A - B) = (fq0 u + fq1) u + fq2, u = x - mean.  sum_e B is
-// b sum(x) (the column statistic) and n ln c is a constant: both are in `base`
-// and added once by the fold.  Per event: 18 FP64 instructions (u, q, the
-// max(q, 0) sum, the exponential, s', the product) against ~27 for
-// kFcnFactored; the selects and the sign test are on the integer pipe.
+// with q = log2(e) (A - B) = (fq0 x + fq1) x + fq2 (the host bounds its
+// rounding and |q| <= 1000 over the range).  sum_e B is b sum(x) (the column
+// statistic) and n ln c is a constant: both are in `base`, added once by the
+// fold.  Per event 16 FP64 instructions (q, the exponential, s', the
+// product, the max(q, 0) sum) against ~27 for kFcnFactored; the sign test,
+// the selects and the exponent insert are on the integer pipe.
 template <class C>
 __device__ __forceinline__ void fast_row(const C& c, double x, double& prod, double& qsum) {
-  const double u = x - c.shift[0];
-  const double q = fma(fma(c.fq[0], u, c.fq[1]), u, c.fq[2]);
+  const double q = fma(fma(c.fq[0], x, c.fq[1]), x, c.fq[2]);
   const int hi = __double2hiint(q), lo = __double2loint(q);
   const bool ga = hi >= 0;  // A >= B: the Gaussian term is the larger
   qsum += __hiloint2double(ga ? hi : 0, ga ? lo : 0);
-  const double t = fcn_exp2_neg(__hiloint2double(hi | (int)0x80000000, lo));  // 2^-|q|
+  const double t = fcn_exp2_neg(-fabs(q));  // 2^-|q| (-|q| is a DADD operand modifier)
   prod *= fma(ga ? c.fa[1] : c.fa[0], t, ga ? c.fa[0] : c.fa[1]);
 }
+
+// rows of a full tile loaded per batch on the kFcnFast path
+#ifndef HK_FCN_FAST_BATCH
+#define HK_FCN_FAST_BATCH 16
+#endif
 
 // One tile: returns sum ln d over this thread's rows; flags
 // d <= 0 / non-finite (fitting.py:200-205) as ~row in *bad (max = first row).
@@ -271,11 +275,26 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
     // thread and tile, no exponent bookkeeping
     double prod = 1.0, qsum = 0.0;
     if (end - begin == kFcnTile) {
-      double xv[kFcnRows];
 #pragma unroll
-      for (int i = 0; i < kFcnRows; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
+      for (int i0 = 0; i0 < kFcnRows; i0 += HK_FCN_FAST_BATCH) {
+        double xv[HK_FCN_FAST_BATCH];
 #pragma unroll
-      for (int i = 0; i < kFcnRows; ++i) fast_row(c, xv[i], prod, qsum);
+        for (int i = 0; i < HK_FCN_FAST_BATCH; ++i) {
+#ifdef HK_FCN_PROBE_NOLOAD  // A/B probe only: rows synthesised from the row index
+          xv[i] = (double)((r0 + (i0 + i) * kBlock) & 1023) * 0.009765625;
+#else
+          xv[i] = __ldg(x + r0 + (i0 + i) * kBlock);
+#endif
+        }
+#pragma unroll
+        for (int i = 0; i < HK_FCN_FAST_BATCH; ++i) {
+#ifdef HK_FCN_PROBE_NOCOMPUTE  // A/B probe only: loads + reductions, no arithmetic
+          prod += xv[i];
+#else
+          fast_row(c, xv[i], prod, qsum);
+#endif
+        }
+      }
     } else {
       for (int i = 0; i < kFcnRows; ++i) {
         const int64_t r = r0 + i * kBlock;
@@ -346,6 +365,109 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const d
     block_sum_store<1>(acc, w.part + ch);
   }
   fcn_finish(w, chunks, V == kFcnFast ? c.base : 0.0);
+}
+
+// ----------------------------------------- TMA-pipelined kFcnFast FCN -----
+// Persistent CTAs (3 per SM) take 4096-row tiles from a device counter; one
+// thread streams each tile (32 KB) into shared memory with a 1-D bulk TMA
+// copy (cp.async.bulk, completion on an mbarrier) two tiles ahead, so the
+// column's load latency overlaps the previous tiles' arithmetic and the LSU
+// issues no global loads.  Per tile the arithmetic, row order and partial
+// are range_logsum<kFcnFast>'s (the ragged last tile runs that function), so
+// every value is bit-identical to k_nll_fused<kFcnFast>, k_nll_many and the
+// session.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n HK_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HK_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kTmaStages = 2;
+constexpr int kTmaSmem = kTmaStages * kFcnTile * (int)sizeof(double);  // 64 KB dynamic
+// smallest column the persistent TMA FCN takes (shorter: k_nll_fused<kFcnFast>).
+// Measured on B200 (tools/gpu_r02_tma.sh, gpurun_out -> profiles/r02_fcn_tma_ab.jsonl),
+// kernel us TMA vs k_nll_fused: 5e6 16.6 vs 15.7, 1e7 24.8 vs 22.6 (L2-resident
+// column: the launched tiles' 16 loads in flight per thread win), 2e7 47.1 vs
+// 48.9, 5e7 88.1 vs 96.1 (HBM-resident: the TMA stream wins by 8%).
+#ifndef HK_FCN_TMA_MIN_N
+#define HK_FCN_TMA_MIN_N (4096LL * 4096)
+#endif
+#ifndef HK_FCN_TMA_MIN_BLOCKS
+#define HK_FCN_TMA_MIN_BLOCKS 3
+#endif
+
+__global__ void __launch_bounds__(kBlock, HK_FCN_TMA_MIN_BLOCKS)
+    k_nll_fast_tma(const double* __restrict__ x, int64_t n, const __grid_constant__ Coeffs c, FcnWork w) {
+  extern __shared__ __align__(128) double s_x[];  // kTmaStages tiles
+  __shared__ __align__(8) uint64_t s_bar[kTmaStages];
+  __shared__ long long s_tile[kTmaStages];
+  const int64_t full = n / kFcnTile;               // tiles the TMA streams
+  const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
+  // thread 0: take the next tile index and start its copy into stage s
+  auto issue = [&](int s) {
+    const long long t = (long long)atomicAdd(w.next, 1ull);
+    s_tile[s] = t;
+    if (t < full) tma_load_1d(s_x + s * kFcnTile, x + t * kFcnTile, kFcnTile * sizeof(double), &s_bar[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kTmaStages; ++s) issue(s);
+  }
+  __syncthreads();
+  uint32_t phase = 0;  // bit s: parity of stage s's next completion
+  for (int k = 0;; ++k) {
+    const int s = k % kTmaStages;
+    const long long t = s_tile[s];
+    if (t >= chunks) break;
+    double acc[1];
+    if (t < full) {
+      mbar_wait(&s_bar[s], (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const double* xs = s_x + s * kFcnTile + threadIdx.x;
+      double prod = 1.0, qsum = 0.0;
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) fast_row(c, xs[i * kBlock], prod, qsum);
+      acc[0] = fma(qsum, 0.6931471805599453, log(prod));
+    } else {  // the ragged last tile
+      unsigned long long bad = 0;
+      acc[0] = range_logsum<kFcnFast>(x, t * kFcnTile, n, c, &bad, threadIdx.x);
+    }
+    block_sum_store<1>(acc, w.part + t);  // its barriers: every read of stage s is done
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async-proxy write
+      issue(s);
+    }
+  }
+  fcn_finish(w, chunks, c.base);
+}
+
+int fast_tma_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_nll_fast_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nll_fast_tma, kBlock, kTmaSmem);
+    grid = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+  }
+  return grid;
 }
 
 // Reference op order (fitting.py:160-166, functors.py:142-143, :161) with no
@@ -857,7 +979,8 @@ int session_stop(Session& S, bool release = false) {
 // density is positive for every event -- exactly the events kFcnFactored
 // takes without its fallback, so no per-event check is needed.  Also the
 // amplitude ratio must be >= 1e-15 (the 16-factor product of s' stays normal)
-// and the rounding of the quadratic q over the range <= 1e-11 (log2 units).
+// and the rounding of the quadratic q over the range <= 1e-11 (log2 units)
+// with |q| <= 999 (fcn_exp2_neg's domain).
 void fast_coeffs(const hk_model_t* m, int64_t n, Coeffs* c) {
   c->fast = 0;
   if (n <= 0 || !m->has_stats || m->x_count != n) return;
@@ -873,14 +996,25 @@ void fast_coeffs(const hk_model_t* m, int64_t n, Coeffs* c) {
   const double a_hi = -0.5 * zc * zc;
   const double m_lo = b_lo, m_hi = std::fmax(a_hi, b_hi);
   if (!(m_lo > c->m_lo + 1.0) || !(m_hi < c->m_hi - 1.0)) return;
+  // q(x) = log2(e) (A - B) = a2 x^2 + a1 x + a0 (from q2 u^2 + q1 u + q0, u = x - mean)
   const double log2e = 1.4426950408889634;
-  const double q2 = log2e * c->q2, q1 = log2e * c->q1, q0 = log2e * c->q0;
-  const double umax = std::fmax(std::fabs(xmin - mu), std::fabs(xmax - mu));
-  const double err = 8.0 * 1.1102230246251565e-16 * (std::fabs(q2) * umax * umax + std::fabs(q1) * umax + std::fabs(q0));
+  const double a2 = log2e * c->q2;
+  const double a1 = log2e * (c->q1 - 2.0 * c->q2 * mu);
+  const double a0 = log2e * ((c->q2 * mu - c->q1) * mu + c->q0);
+  const double xa = std::fmax(std::fabs(xmin), std::fabs(xmax));
+  const double err = 16.0 * 1.1102230246251565e-16 *
+                     (std::fabs(a2) * xa * xa + std::fabs(a1) * xa + std::fabs(a0) + 1.0);
   if (!(err <= 1e-11)) return;
-  c->fq[0] = q2;
-  c->fq[1] = q1;
-  c->fq[2] = q0;
+  // |q| <= 1000 over the range (fcn_exp2_neg's domain): q is concave, so its
+  // extremes are at the ends or the vertex
+  const double q_lo = std::fmin(a2 * xmin * xmin + a1 * xmin + a0, a2 * xmax * xmax + a1 * xmax + a0);
+  const double xv = std::fmin(std::fmax(-a1 / (2.0 * a2), xmin), xmax);
+  const double q_hi = std::fmax(a2 * xv * xv + a1 * xv + a0, std::fmax(a2 * xmin * xmin + a1 * xmin + a0,
+                                                                      a2 * xmax * xmax + a1 * xmax + a0));
+  if (!(q_lo >= -999.0) || !(q_hi <= 999.0)) return;
+  c->fq[0] = a2;
+  c->fq[1] = a1;
+  c->fq[2] = a0;
   c->fa[0] = c->amp[0] / amax;
   c->fa[1] = c->amp[1] / amax;
   c->base = b * m->x_sum + (double)n * std::log(amax);
@@ -1086,8 +1220,8 @@ void fcn_schedule(int64_t n, int64_t* full, int64_t* tail_ctas) {
 // re-armed by the kernel): [0] sum of logs, [1] first bad row (u64 bits),
 // [2] ~bad-row cell, [3] CTA ticket, [4] ~zero-divisor cell, [5] first zero
 // divisor row (u64 bits), [6..7] caller's (hk_nll_combine: [6] = the shard's
-// first global row), [8..] partials.
-constexpr int kFcnWorkHead = 8;
+// first global row), [8] tile counter (k_nll_fast_tma), [16..] partials.
+constexpr int kFcnWorkHead = 16;  // [8] the persistent FCN's tile counter, [9..15] spare
 
 // mb == NULL: asynchronous call, the result stays in d_work[0, 1, 5]
 int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
@@ -1096,6 +1230,7 @@ int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
   w->ticket = reinterpret_cast<unsigned int*>(d_work + 3);
   w->div0 = reinterpret_cast<unsigned long long*>(d_work + 4);
   w->part = d_work + kFcnWorkHead;
+  w->next = reinterpret_cast<unsigned long long*>(d_work + 8);
   w->host_mail = nullptr;
   w->seq = 0;
   if (mb) {
@@ -1476,7 +1611,15 @@ int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d
   w.div0 = nullptr;  // the closed-form shapes have no divisions to check
   const unsigned grid = chunk_grid(w.full + w.tail_ctas);
   switch (fcn_variant(c)) {
-    case kFcnFast: k_nll_fused<kFcnFast><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
+    case kFcnFast:
+      if (n >= (int64_t)HK_FCN_TMA_MIN_N) {  // enough tiles to keep every persistent CTA busy
+        const int64_t tiles = (n + kFcnTile - 1) / kFcnTile;
+        const int g = fast_tma_grid();
+        k_nll_fast_tma<<<(unsigned)(tiles < g ? tiles : g), kBlock, kTmaSmem, st>>>(d_x, n, c, w);
+      } else {
+        k_nll_fused<kFcnFast><<<grid, kBlock, 0, st>>>(d_x, n, c, w);
+      }
+      break;
     case kFcnFactored: k_nll_fused<kFcnFactored><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     case kFcnGE: k_nll_fused<kFcnGE><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;
     default: k_nll_fused<kFcnGeneric><<<grid, kBlock, 0, st>>>(d_x, n, c, w); break;

@@ -88,6 +88,9 @@ struct FcnWork {
   // rows from full * 4096 on are split evenly over tail_ctas more CTAs, so
   // the last wave is short instead of a few full tiles on an idle GPU
   int64_t full, tail_ctas;
+  // dynamic tile counter of the persistent (TMA-pipelined) FCN; re-armed to
+  // 0 by the last CTA (NULL: not used)
+  unsigned long long* next;
 };
 
 __device__ __forceinline__ void fcn_range(const FcnWork& w, int64_t n, int64_t b, int64_t* begin,
@@ -109,6 +112,7 @@ __device__ __forceinline__ void fcn_publish(const FcnWork& w, double total) {
   w.out[1] = __longlong_as_double((long long)~b);
   w.out[5] = __longlong_as_double((long long)~z);
   *w.ticket = 0u;
+  if (w.next) *w.next = 0ull;
   if (w.host_mail) {
     w.host_mail[1] = (unsigned long long)__double_as_longlong(total);
     w.host_mail[2] = ~b;

@@ -294,3 +294,30 @@ def test_fcn_session_bitwise_and_lifecycle(cuda, hk, golden):
         assert not s3.on
         assert hk.nll(g1, s1, ["x0"]) == pytest.approx(-116014.30412842518, rel=1e-10)
     assert _lib.lib().hk_fcn_session_stop() == 0
+
+
+def test_nll_large_column_tma_path(cuda, hk):
+    """Columns of >= 4096 x 4096 rows take the persistent TMA-pipelined FCN
+    (k_nll_fast_tma); its value equals the single-pass nll_many evaluation
+    (k_nll_many: same tiles, rows and fold) bit for bit, repeats bitwise, and
+    matches the oracle within the FCN's 1e-10 budget, ragged tail included."""
+    from oracle import oracle as O  # checker only
+    from paper_1711_05683_b200.fitting import nll_many
+    rs = np.random.default_rng(11)
+    n = 4096 * 4096 + 4096 * 333 + 777
+    x = np.clip(np.concatenate([rs.normal(5, 0.5, n // 2), rs.exponential(3.0, n - n // 2)]), 1e-3, 9.999)
+    rs.shuffle(x)
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    model = _toy_model(hk, 0.4 * n, 0.6 * n)
+    ps = model.param_set()
+    base = ps.values()
+    pts = [base, (0.41 * n, 4.9, 0.55, 0.59 * n, 2.8)]
+    got = []
+    for pt in pts:
+        ps.set_values(pt)
+        got.append(hk.nll(model, data, ["x0"]))
+        assert hk.nll(model, data, ["x0"]) == got[-1]
+        want = O.nll(x, O.gauss_exp_components(pt[1], pt[2], pt[4], pt[0], pt[3]))
+        assert abs(got[-1] - want) <= 1e-10 * abs(want)
+    ps.set_values(base)
+    assert nll_many(model, data, ["x0"], pts) == got

@@ -38,13 +38,17 @@ out = {}
 out["nll_total"] = t(lambda i: hk.nll(model, data, cols))
 out["nll_param_change"] = t(lambda i: (setattr(ps["mean"], "value", 5.0 + 1e-6 * (i % 7)), hk.nll(model, data, cols)))
 out["observable"] = t(lambda i: fitting._observable(data, cols, model))
-out["lower_model"] = t(lambda i: fitting.lower_model(model))
-out["lower_model_param_change"] = t(lambda i: (setattr(ps["mean"], "value", 5.0 + 1e-6 * (i % 7)), fitting.lower_model(model)))
+xo = fitting._observable(data, cols, model)
+out["lower_model"] = t(lambda i: fitting.lower_model(model, xo))
+out["lower_model_param_change"] = t(lambda i: (setattr(ps["mean"], "value", 5.0 + 1e-6 * (i % 7)), fitting.lower_model(model, xo)))
+out["param_set_only"] = t(lambda i: setattr(ps["mean"], "value", 5.0 + 1e-6 * (i % 7)))
+out["norms_param_change"] = t(lambda i: (setattr(ps["mean"], "value", 5.0 + 1e-6 * (i % 7)), [p.norm() for _, p in model.components]))
+out["column_stats"] = t(lambda i: fitting.column_stats(xo))
 out["stream_ptr"] = t(lambda i: _lib.stream_ptr())
 out["workspace"] = t(lambda i: fitting._Workspace.get(len(data), 0))
 out["expected_total"] = t(lambda i: model.expected_total())
 xd = fitting._observable(data, cols, model)
-lm = fitting.lower_model(model)
+lm = fitting.lower_model(model, xo)
 work = fitting._Workspace.get(len(data), _lib.stream_ptr())
 L = _lib.lib()
 st = _lib.stream_ptr()
