@@ -89,6 +89,30 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
   return out;
 }
 
+// The same rounds with the key schedule precomputed per launch (rk[2r],
+// rk[2r + 1] = round r's two key words): the round keys are kernel-parameter
+// (constant-bank) operands of the LOP3s, so the 20 key additions and their
+// registers leave the per-event code.  Bit-identical to philox4x32_10.
+__device__ __forceinline__ Philox4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                    const uint32_t (&rk)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  Philox4 out;
+  out.v[0] = c0;
+  out.v[1] = c1;
+  out.v[2] = c2;
+  out.v[3] = c3;
+  return out;
+}
+
 constexpr uint32_t kPhiloxTag = 0x686b7068u;  // "hkph": separates this use of the key
 
 // Per-launch RNG parameters; both modes are derived from the same hk_key_t.
@@ -96,6 +120,7 @@ struct RngParams {
   uint64_t base;  // SplitMix64 key base (reference mode) / Philox key (philox mode)
   uint64_t kc;    // key.counter
   int32_t mode;
+  uint32_t rk[20];  // philox mode: the round keys of `base` (philox4x32_10_rk)
 };
 
 inline RngParams make_rng(const hk_key_t& k) {
@@ -103,6 +128,13 @@ inline RngParams make_rng(const hk_key_t& k) {
   r.base = key_base(k.seed, k.stream);
   r.kc = k.counter;
   r.mode = k.mode;
+  uint32_t k0 = (uint32_t)r.base, k1 = (uint32_t)(r.base >> 32);
+  for (int i = 0; i < 10; ++i) {
+    r.rk[2 * i] = k0;
+    r.rk[2 * i + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
   return r;
 }
 
@@ -117,11 +149,9 @@ __device__ __forceinline__ void draw_bits(const RngParams& rp, uint64_t row, uin
     for (int j = 0; j < D; ++j) bits[j] = mix64(x0 + (uint64_t)j * kGolden) >> 11;
   } else {
     const uint64_t ev = row + rp.kc;
-    const uint32_t k0 = (uint32_t)rp.base, k1 = (uint32_t)(rp.base >> 32);
 #pragma unroll
     for (int b = 0; b < (D + 1) / 2; ++b) {
-      const Philox4 o = philox4x32_10((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)b, kPhiloxTag,
-                                      k0, k1);
+      const Philox4 o = philox4x32_10_rk((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)b, kPhiloxTag, rp.rk);
       bits[2 * b] = (((uint64_t)o.v[0] << 32) | o.v[1]) >> 11;
       if (2 * b + 1 < D) bits[2 * b + 1] = (((uint64_t)o.v[2] << 32) | o.v[3]) >> 11;
     }
@@ -135,8 +165,7 @@ __device__ __forceinline__ uint64_t draw_bit_rt(const RngParams& rp, uint64_t ro
     return mix64(rp.base + ((row + rp.kc) * (uint64_t)D + (uint64_t)j) * kGolden) >> 11;
   } else {
     const uint64_t ev = row + rp.kc;
-    const Philox4 o = philox4x32_10((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)(j >> 1),
-                                    kPhiloxTag, (uint32_t)rp.base, (uint32_t)(rp.base >> 32));
+    const Philox4 o = philox4x32_10_rk((uint32_t)ev, (uint32_t)(ev >> 32), (uint32_t)(j >> 1), kPhiloxTag, rp.rk);
     return (j & 1) ? ((((uint64_t)o.v[2] << 32) | o.v[3]) >> 11)
                    : ((((uint64_t)o.v[0] << 32) | o.v[1]) >> 11);
   }

@@ -585,8 +585,7 @@ __global__ void k_rng(RngParams rp, const uint64_t* ctr, int64_t n, uint64_t* ra
     if (raw) raw[i] = r;
     bits = r >> 11;
   } else {
-    const Philox4 o = philox4x32_10((uint32_t)c, (uint32_t)(c >> 32), 0u, kPhiloxTag,
-                                    (uint32_t)rp.base, (uint32_t)(rp.base >> 32));
+    const Philox4 o = philox4x32_10_rk((uint32_t)c, (uint32_t)(c >> 32), 0u, kPhiloxTag, rp.rk);
     const uint64_t r = ((uint64_t)o.v[0] << 32) | o.v[1];
     if (raw) raw[i] = r;
     bits = r >> 11;
