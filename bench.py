@@ -60,11 +60,16 @@ def _fp64_roofline(kernel: str, events_per_s_per_gpu: float, note: str = "") -> 
     SURVEY.md 8(d)): the live per-GPU event rate x the kernel's DP instructions
     per event (ncu, committed) against the DFMA instruction rate measured by
     tools/fp64_peak.cu (committed; MEASURED_PEAKS.json has no FP64 figure)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_fp64_roofline.json")) as fh:
-            d = json.load(fh)
-        k, pk = d["kernels"][kernel], d["peak"]
-    except (OSError, KeyError, ValueError):
+    d = None
+    for tag in ("r02", "r01"):   # the newest committed DP-count capture
+        try:
+            with open(os.path.join(ROOT, "profiles", f"{tag}_fp64_roofline.json")) as fh:
+                d = json.load(fh)
+            k, pk = d["kernels"][kernel], d["peak"]
+            break
+        except (OSError, KeyError, ValueError):
+            d = None
+    if d is None:
         return None
     inst = events_per_s_per_gpu * k["dp_inst_per_event"]
     return {"bound": "fp64", "achieved": inst * 1e-12, "peak": pk["dp_inst_per_s"] * 1e-12,
@@ -380,6 +385,11 @@ def fcn_bench(hk, torch, evals: int = 200, rank: int = 0, world: int = 1, dist=N
            "unit": "evals/s", "n_gpus": world, "scaling": "strong", "us_per_eval": dt * 1e6,
            "kernel_us": kt * 1e6, "c_abi_us": ct * 1e6,
            "roofline": _fp64_roofline("k_nll_fused", n_local / kt)}
+    peak = _peaks()
+    if out["roofline"]:
+        # the same kernel against HBM: 8 B read per event (the observable column)
+        out["roofline"]["hbm_view"] = {"achieved_GBps": 8 * n_local / kt / 1e9, "peak_GBps": peak["hbm_gbs"],
+                                       "frac": 8 * n_local / kt / 1e9 / peak["hbm_gbs"]}
     if world == 1:
         out.update(fcn_minimiser_paths(hk, torch, model, data, points, (mean, sigma, tau), evals))
     return out
