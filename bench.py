@@ -121,8 +121,15 @@ class NvmlClockSampler:
                 k += 1
                 time.sleep(0.0005)
 
+        # the timed loop only enqueues work and then waits: a short GIL
+        # switch interval lets the poller run while the main thread holds it
+        import sys
+        self.switch = sys.getswitchinterval()
+        sys.setswitchinterval(1e-4)
         self.thread = threading.Thread(target=poll, daemon=True)
         self.thread.start()
+        while not self.samples and self.thread.is_alive():   # first sample before the region
+            time.sleep(0.0002)
         return self
 
     def __exit__(self, *exc):
@@ -130,6 +137,8 @@ class NvmlClockSampler:
             return self.fallback.__exit__(*exc)
         self.stop.set()
         self.thread.join(timeout=5)
+        import sys
+        sys.setswitchinterval(self.switch)
 
     def summary(self) -> dict:
         if not self.ok:
