@@ -17,6 +17,8 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #if defined(__SSE2__)
 #include <emmintrin.h>
 #endif
@@ -356,7 +358,8 @@ template <int V>
 __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const double* __restrict__ x, int64_t n,
                                                       const __grid_constant__ Coeffs c, FcnWork w) {
   const int64_t chunks = w.full + w.tail_ctas;
-  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < chunks; b += gridDim.x) {
+    const int64_t ch = fcn_tile(w, b, chunks);
     unsigned long long bad = 0;
     int64_t begin, end;
     fcn_range(w, n, ch, &begin, &end);
@@ -418,10 +421,13 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_TMA_MIN_BLOCKS)
   const int64_t full = n / kFcnTile;               // tiles the TMA streams
   const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
   // thread 0: take the next tile index and start its copy into stage s
+  // s_tile: the tile in this call's scan direction, or -1 once the counter
+  // has passed the last one
   auto issue = [&](int s) {
-    const long long t = (long long)atomicAdd(w.next, 1ull);
+    const long long u = (long long)atomicAdd(w.next, 1ull);
+    const long long t = u < chunks ? (long long)fcn_tile(w, u, chunks) : -1;
     s_tile[s] = t;
-    if (t < full) tma_load_1d(s_x + s * kFcnTile, x + t * kFcnTile, kFcnTile * sizeof(double), &s_bar[s]);
+    if (t >= 0 && t < full) tma_load_1d(s_x + s * kFcnTile, x + t * kFcnTile, kFcnTile * sizeof(double), &s_bar[s]);
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s)
@@ -434,7 +440,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_TMA_MIN_BLOCKS)
   for (int k = 0;; ++k) {
     const int s = k % kTmaStages;
     const long long t = s_tile[s];
-    if (t >= chunks) break;
+    if (t < 0) break;
     double acc[1];
     if (t < full) {
       mbar_wait(&s_bar[s], (phase >> s) & 1u);
@@ -576,6 +582,7 @@ struct ManyArgs {
   unsigned int* done;            // groups folded
   volatile unsigned long long* host_mail;
   unsigned long long seq;
+  int32_t rev;                   // the first group's scan direction (flipped per call)
   FPoint pt[HK_MAX_POINTS];  // k points, padded with copies of the last to kpad
 };
 
@@ -585,8 +592,11 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
   __shared__ double tot[kManyG];
   const int64_t total = a.tiles * a.groups;
   for (int64_t b = blockIdx.x; b < total; b += gridDim.x) {
-    const int64_t t = b % a.tiles;
     const int g = (int)(b / a.tiles);
+    // serpentine: group g walks the tiles in the direction opposite to group
+    // g - 1 (and to the previous call's last group), so each group's pass
+    // starts on the L2-resident end of the column
+    const int64_t t = ((g & 1) ^ a.rev) ? a.tiles - 1 - b % a.tiles : b % a.tiles;
     const int64_t begin = t * kFcnTile;
     const int64_t end = begin + kFcnTile < a.n ? begin + kFcnTile : a.n;
     const int64_t r0 = begin + threadIdx.x;
@@ -1223,6 +1233,25 @@ void fcn_schedule(int64_t n, int64_t* full, int64_t* tail_ctas) {
 // first global row), [8] tile counter (k_nll_fast_tma), [16..] partials.
 constexpr int kFcnWorkHead = 16;  // [8] the persistent FCN's tile counter, [9..15] spare
 
+// Scan direction of the next pass over the column behind workspace `key`:
+// alternates per call (a pass of `passes` sweeps ends in the direction it
+// started if passes is even), so consecutive calls meet in L2.  A hint only
+// -- values do not depend on it.
+#ifndef HK_FCN_FLIP
+#define HK_FCN_FLIP 1
+#endif
+int32_t fcn_flip(const void* key, int passes = 1) {
+  if (!HK_FCN_FLIP) return 0;
+  static std::mutex mu;
+  static std::unordered_map<const void*, int32_t> dir;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dir.size() > 4096) dir.clear();
+  int32_t& d = dir[key];
+  const int32_t cur = d;
+  d ^= passes & 1;
+  return cur;
+}
+
 // mb == NULL: asynchronous call, the result stays in d_work[0, 1, 5]
 int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
   w->out = d_work;
@@ -1239,6 +1268,7 @@ int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
     w->seq = ++(*mb)->seq;
   }
   fcn_schedule(n, &w->full, &w->tail_ctas);
+  w->rev = fcn_flip(d_work);
   return HK_OK;
 }
 
@@ -1683,6 +1713,7 @@ int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int
   if (int rc = mailbox(&mb)) return rc;
   a.host_mail = mb->d;
   a.seq = ++mb->seq;
+  a.rev = fcn_flip(d_work, a.groups);
   cudaStream_t st = as_stream(stream);
   if (variant == kFcnFast)
     k_nll_many<kFcnFast><<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);

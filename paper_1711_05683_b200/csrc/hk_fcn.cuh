@@ -91,7 +91,18 @@ struct FcnWork {
   // dynamic tile counter of the persistent (TMA-pipelined) FCN; re-armed to
   // 0 by the last CTA (NULL: not used)
   unsigned long long* next;
+  // scan direction: 1 walks the tiles last to first.  The host flips it on
+  // every call over the same workspace (fcn_flip), so each pass starts on the
+  // tiles the previous pass touched last -- the ones still in L2 -- instead
+  // of cycling through a column larger than L2 in LRU order (1e7 events:
+  // 8% L2 hits).  Tile partials keep their index, so values do not change.
+  int32_t rev;
 };
+
+// the tile a CTA's b-th unit covers in this call's scan direction
+__device__ __forceinline__ int64_t fcn_tile(const FcnWork& w, int64_t b, int64_t tiles) {
+  return w.rev ? tiles - 1 - b : b;
+}
 
 __device__ __forceinline__ void fcn_range(const FcnWork& w, int64_t n, int64_t b, int64_t* begin,
                                           int64_t* end) {
@@ -149,7 +160,8 @@ __device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks, dou
 template <class Dens>
 __device__ __forceinline__ void fcn_density_pass(const FcnWork& w, int64_t n, const Dens& dens) {
   const int64_t chunks = w.full + w.tail_ctas;
-  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < chunks; b += gridDim.x) {
+    const int64_t ch = fcn_tile(w, b, chunks);
     int64_t begin, end;
     fcn_range(w, n, ch, &begin, &end);
     unsigned long long bad = 0, zero = 0;
