@@ -41,8 +41,8 @@ struct Coeffs {
   // q0: A - B as a quadratic in x - mean
   double m_lo, m_hi;
   double q2, q1, q0;
-  // kFcnFast (fast_coeffs): amplitudes over their max c, log2(e) (A - B) as a
-  // quadratic in x - mean, and base = sum_e B(x_e) + n ln c = b sum(x) + n ln c
+  // kFcnFast (fast_coeffs): amplitudes over their max c, q = log2(e) (A - B) as
+  // a quadratic in x, and base = sum_e B(x_e) + n ln c = b sum(x) + n ln c
   double fa[2], fq[3], base;
   int32_t fast;
 };
@@ -200,12 +200,12 @@ __constant__ double kExp2Poly[9] = {1.328492507863422e-06,  1.5308981596230215e-
                                     0.001333345520138187,   0.009618129182690833,   0.05550410935556957,
                                     0.2402265069621877,     0.6931471805476419,     0.9999999999999317};
 
-// 2^y for -1000 <= y <= 0 (the host proves the range, fast_coeffs): 2^n 2^f,
+// 2^y for -1000 <= y <= 60 (the host proves the range, fast_coeffs): 2^n 2^f,
 // n = rint(y), f in [-1/2, 1/2], n added to the high word (2^f is normal and
-// 2^n >= 2^-1000, so the result is a normal double, no underflow path).
+// 2^n in [2^-1000, 2^60], so the result is a normal double, no special path).
 // Moves each density by <= 2.9e-12 relative: summed over 1e7 events at most
 // 3e-5 of ln L, ~1e-13 relative -- the FCN's budget is 1e-10.
-__device__ __forceinline__ double fcn_exp2_neg(double y) {
+__device__ __forceinline__ double fcn_exp2(double y) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52: rounds y to an integer
   const double r = y + magic;
   const double f = y - (r - magic);
@@ -216,24 +216,21 @@ __device__ __forceinline__ double fcn_exp2_neg(double y) {
   return __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
 }
 
-// One event of the kFcnFast FCN.  The host (fast_coeffs) has proved over the
-// column's [min, max] that both reference terms are finite normal doubles and
-// that the density is positive, so there is no per-event check; ln d is
-//   ln d = B + max(A - B, 0) + ln c + ln s',  s' = fa_big + fa_small 2^-|q|,
-// with q = log2(e) (A - B) = (fq0 x + fq1) x + fq2 (the host bounds its
-// rounding and |q| <= 1000 over the range).  sum_e B is b sum(x) (the column
-// statistic) and n ln c is a constant: both are in `base`, added once by the
-// fold.  Per event 16 FP64 instructions (q, the exponential, s', the
-// product, the max(q, 0) sum) against ~27 for kFcnFactored; the sign test,
-// the selects and the exponent insert are on the integer pipe.
+// One event of the kFcnFast FCN.  With A = -((x - mean)/sigma)^2 / 2 and
+// B = b x the two reference terms are amp0 e^A and amp1 e^B, so
+//   d = c e^B s',  s' = fa1 + fa0 2^q,  q = log2(e) (A - B) = (fq0 x + fq1) x + fq2,
+// c = max(amp0, amp1), fa = amp / c.  The host (fast_coeffs) has proved over
+// the column's [min, max] that both reference terms are finite normal
+// doubles, that the density is positive and that -1000 <= q <= 60, so there
+// is no per-event check and no select: s' lies in [1e-15, 1 + 2^60] and a
+// product of 16 of them stays a normal double.  ln d = B + ln c + ln s';
+// sum_e B = b sum(x) (the column statistic) and n ln c are constants added
+// once by the fold (`base`).  Per event 15 FP64 instructions (q, the
+// exponential, s', the product); the exponent insert is on the integer pipe.
 template <class C>
-__device__ __forceinline__ void fast_row(const C& c, double x, double& prod, double& qsum) {
+__device__ __forceinline__ void fast_row(const C& c, double x, double& prod) {
   const double q = fma(fma(c.fq[0], x, c.fq[1]), x, c.fq[2]);
-  const int hi = __double2hiint(q), lo = __double2loint(q);
-  const bool ga = hi >= 0;  // A >= B: the Gaussian term is the larger
-  qsum += __hiloint2double(ga ? hi : 0, ga ? lo : 0);
-  const double t = fcn_exp2_neg(-fabs(q));  // 2^-|q| (-|q| is a DADD operand modifier)
-  prod *= fma(ga ? c.fa[1] : c.fa[0], t, ga ? c.fa[0] : c.fa[1]);
+  prod *= fma(c.fa[0], fcn_exp2(q), c.fa[1]);
 }
 
 // rows of a full tile loaded per batch on the kFcnFast path
@@ -275,7 +272,7 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
   if constexpr (V == kFcnFast) {
     // the product of <= 16 factors s' in [1e-15, 2] stays normal: one log per
     // thread and tile, no exponent bookkeeping
-    double prod = 1.0, qsum = 0.0;
+    double prod = 1.0;
     if (end - begin == kFcnTile) {
 #pragma unroll
       for (int i0 = 0; i0 < kFcnRows; i0 += HK_FCN_FAST_BATCH) {
@@ -293,17 +290,17 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
 #ifdef HK_FCN_PROBE_NOCOMPUTE  // A/B probe only: loads + reductions, no arithmetic
           prod += xv[i];
 #else
-          fast_row(c, xv[i], prod, qsum);
+          fast_row(c, xv[i], prod);
 #endif
         }
       }
     } else {
       for (int i = 0; i < kFcnRows; ++i) {
         const int64_t r = r0 + i * kBlock;
-        if (r < end) fast_row(c, __ldg(x + r), prod, qsum);
+        if (r < end) fast_row(c, __ldg(x + r), prod);
       }
     }
-    return fma(qsum, 0.6931471805599453, log(prod));
+    return log(prod);
   }
   LogProd lp;
   double msum = 0.0;
@@ -446,10 +443,10 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_TMA_MIN_BLOCKS)
       mbar_wait(&s_bar[s], (phase >> s) & 1u);
       phase ^= 1u << s;
       const double* xs = s_x + s * kFcnTile + threadIdx.x;
-      double prod = 1.0, qsum = 0.0;
+      double prod = 1.0;
 #pragma unroll
-      for (int i = 0; i < kFcnRows; ++i) fast_row(c, xs[i * kBlock], prod, qsum);
-      acc[0] = fma(qsum, 0.6931471805599453, log(prod));
+      for (int i = 0; i < kFcnRows; ++i) fast_row(c, xs[i * kBlock], prod);
+      acc[0] = log(prod);
     } else {  // the ragged last tile
       unsigned long long bad = 0;
       acc[0] = range_logsum<kFcnFast>(x, t * kFcnTile, n, c, &bad, threadIdx.x);
@@ -615,12 +612,9 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
     const FPoint* c = a.pt + g * kManyG;  // padded to kpad points on the host
     if constexpr (V == kFcnFast) {
       // per point exactly range_logsum<kFcnFast>'s chain: same values
-      double prod[kManyG], qsum[kManyG];
+      double prod[kManyG];
 #pragma unroll
-      for (int j = 0; j < kManyG; ++j) {
-        prod[j] = 1.0;
-        qsum[j] = 0.0;
-      }
+      for (int j = 0; j < kManyG; ++j) prod[j] = 1.0;
       if (full) {
         double xv[kFcnRows];
 #pragma unroll
@@ -628,7 +622,7 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
 #pragma unroll
         for (int i = 0; i < kFcnRows; ++i) {
 #pragma unroll
-          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xv[i], prod[j], qsum[j]);
+          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xv[i], prod[j]);
         }
       } else {
         for (int i = 0; i < kFcnRows; ++i) {
@@ -636,11 +630,11 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MANY_MIN_BLOCKS) k_nll_many(con
           if (r >= end) continue;
           const double xr = __ldg(a.x + r);
 #pragma unroll
-          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xr, prod[j], qsum[j]);
+          for (int j = 0; j < kManyG; ++j) fast_row(c[j], xr, prod[j]);
         }
       }
 #pragma unroll
-      for (int j = 0; j < kManyG; ++j) msum[j] = fma(qsum[j], 0.6931471805599453, log(prod[j]));
+      for (int j = 0; j < kManyG; ++j) msum[j] = log(prod[j]);
     } else if (full) {
       double xv[kFcnRows];
 #pragma unroll
@@ -988,9 +982,11 @@ int session_stop(Session& S, bool release = false) {
 // margin of 1: then both reference terms are finite normal doubles and the
 // density is positive for every event -- exactly the events kFcnFactored
 // takes without its fallback, so no per-event check is needed.  Also the
-// amplitude ratio must be >= 1e-15 (the 16-factor product of s' stays normal)
-// and the rounding of the quadratic q over the range <= 1e-11 (log2 units)
-// with |q| <= 999 (fcn_exp2_neg's domain).
+// amplitude ratio must be >= 1e-15 (16-factor products of s' stay normal),
+// the rounding of the quadratic q over the range <= 1e-11 (log2 units), and
+// -999 <= q <= 59 (fcn_exp2's domain, and s' <= 1 + 2^59).  A model whose
+// Gaussian term outgrows the exponential one by more than 2^59 somewhere in
+// the range takes kFcnFactored instead.
 void fast_coeffs(const hk_model_t* m, int64_t n, Coeffs* c) {
   c->fast = 0;
   if (n <= 0 || !m->has_stats || m->x_count != n) return;
@@ -1015,13 +1011,13 @@ void fast_coeffs(const hk_model_t* m, int64_t n, Coeffs* c) {
   const double err = 16.0 * 1.1102230246251565e-16 *
                      (std::fabs(a2) * xa * xa + std::fabs(a1) * xa + std::fabs(a0) + 1.0);
   if (!(err <= 1e-11)) return;
-  // |q| <= 1000 over the range (fcn_exp2_neg's domain): q is concave, so its
+  // -999 <= q <= 59 over the range (fcn_exp2's domain): q is concave, so its
   // extremes are at the ends or the vertex
   const double q_lo = std::fmin(a2 * xmin * xmin + a1 * xmin + a0, a2 * xmax * xmax + a1 * xmax + a0);
   const double xv = std::fmin(std::fmax(-a1 / (2.0 * a2), xmin), xmax);
   const double q_hi = std::fmax(a2 * xv * xv + a1 * xv + a0, std::fmax(a2 * xmin * xmin + a1 * xmin + a0,
                                                                       a2 * xmax * xmax + a1 * xmax + a0));
-  if (!(q_lo >= -999.0) || !(q_hi <= 999.0)) return;
+  if (!(q_lo >= -999.0) || !(q_hi <= 59.0)) return;
   c->fq[0] = a2;
   c->fq[1] = a1;
   c->fq[2] = a0;

@@ -321,3 +321,31 @@ def test_nll_large_column_tma_path(cuda, hk):
         assert abs(got[-1] - want) <= 1e-10 * abs(want)
     ps.set_values(base)
     assert nll_many(model, data, ["x0"], pts) == got
+
+
+@pytest.mark.parametrize("mu,sigma,tau", [(5.0, 0.5, 3.0),      # the check-free kFcnFast path
+                                          (9.0, 0.3, 0.2),      # q reaches ~65 > 59: kFcnFactored
+                                          (1.0, 0.05, 50.0),    # q down to ~-23000: kFcnFactored
+                                          (0.0, 2.0, 1e6)])     # nearly flat background
+def test_nll_regimes_vs_oracle(cuda, hk, mu, sigma, tau):
+    """The Gaussian + exponential FCN against the oracle at 1e-10 in each
+    regime of the host proof (fast_coeffs): inside it the check-free kernel
+    runs, outside it the factored kernel with its per-event fallback; the
+    single-point, batched and repeated evaluations agree bit for bit."""
+    from oracle import oracle as O  # checker only
+    from paper_1711_05683_b200.fitting import nll_many
+    rs = np.random.default_rng(5)
+    n = 4096 * 300 + 123
+    x = rs.uniform(1e-3, 9.999, n)
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(P("mean", mu), P("sigma", sigma))
+    e = hk.shape_exponential(P("tau", tau))
+    model = hk.add_pdfs([P("n_sig", 0.3 * n), P("n_bkg", 0.7 * n)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+    got = hk.nll(model, data, ["x0"])
+    want = O.nll(x, O.gauss_exp_components(mu, sigma, tau, 0.3 * n, 0.7 * n))
+    assert abs(got - want) <= 1e-10 * abs(want)
+    assert hk.nll(model, data, ["x0"]) == got
+    assert nll_many(model, data, ["x0"], [model.param_set().values()] * 3) == [got] * 3
