@@ -16,6 +16,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -233,6 +234,27 @@ __device__ __forceinline__ void fast_row(const C& c, double x, double& prod) {
   prod *= fma(c.fa[0], fcn_exp2(q), c.fa[1]);
 }
 
+// column loads of the kFcnFast tiles (HK_FCN_LD: 0 __ldg; 1 ld.global.nc
+// with an L2 evict_last policy; 2 plain ld.global with evict_last)
+#ifndef HK_FCN_LD
+#define HK_FCN_LD 0
+#endif
+__device__ __forceinline__ double fcn_ldx(const double* p) {
+#if HK_FCN_LD == 0
+  return __ldg(p);
+#else
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  double v;
+#if HK_FCN_LD == 1
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+#else
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+#endif
+  return v;
+#endif
+}
+
 // rows of a full tile loaded per batch on the kFcnFast path
 #ifndef HK_FCN_FAST_BATCH
 #define HK_FCN_FAST_BATCH 16
@@ -282,7 +304,7 @@ __device__ __forceinline__ double range_logsum(const double* __restrict__ x, int
 #ifdef HK_FCN_PROBE_NOLOAD  // A/B probe only: rows synthesised from the row index
           xv[i] = (double)((r0 + (i0 + i) * kBlock) & 1023) * 0.009765625;
 #else
-          xv[i] = __ldg(x + r0 + (i0 + i) * kBlock);
+          xv[i] = fcn_ldx(x + r0 + (i0 + i) * kBlock);
 #endif
         }
 #pragma unroll
@@ -1229,15 +1251,29 @@ void fcn_schedule(int64_t n, int64_t* full, int64_t* tail_ctas) {
 // first global row), [8] tile counter (k_nll_fast_tma), [16..] partials.
 constexpr int kFcnWorkHead = 16;  // [8] the persistent FCN's tile counter, [9..15] spare
 
-// Scan direction of the next pass over the column behind workspace `key`:
-// alternates per call (a pass of `passes` sweeps ends in the direction it
-// started if passes is even), so consecutive calls meet in L2.  A hint only
-// -- values do not depend on it.
+// Scan direction of the next pass over a column of `bytes` behind workspace
+// `key` -- a hint only: tile partials keep their index, so values never
+// depend on it.  Measured on B200 (profiles/r02_fcn_rev_ab.jsonl, steady
+// state, ncu --cache-control none): walking the tiles last to first on
+// every call keeps ~35% of an 80 MB column's sectors in L2 (forward: 8%),
+// 1e7 events 20.3 -> 18.6 us, 1.3e7 26.9 -> 26.6; for columns past ~0.85 of
+// L2 a fixed reverse scan loses (1.5e7: 31.7 vs 28.5 us,
+// profiles/r02_fcn_rev_thr.jsonl) and alternating the direction per call
+// wins instead.  HK_FCN_REV_MAX_BYTES overrides the threshold.
 #ifndef HK_FCN_FLIP
 #define HK_FCN_FLIP 1
 #endif
-int32_t fcn_flip(const void* key, int passes = 1) {
+int32_t fcn_flip(const void* key, int64_t bytes, int passes = 1) {
   if (!HK_FCN_FLIP) return 0;
+  static int64_t rev_max = -1;
+  if (rev_max < 0) {
+    const char* env = std::getenv("HK_FCN_REV_MAX_BYTES");
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    rev_max = env ? std::atoll(env) : (int64_t)(0.85 * (l2 > 0 ? l2 : 0));
+  }
+  if (bytes <= rev_max) return 1;
   static std::mutex mu;
   static std::unordered_map<const void*, int32_t> dir;
   std::lock_guard<std::mutex> lock(mu);
@@ -1264,7 +1300,7 @@ int fcn_setup(double* d_work, int64_t n, FcnWork* w, Mailbox** mb) {
     w->seq = ++(*mb)->seq;
   }
   fcn_schedule(n, &w->full, &w->tail_ctas);
-  w->rev = fcn_flip(d_work);
+  w->rev = fcn_flip(d_work, n * (int64_t)sizeof(double));
   return HK_OK;
 }
 
@@ -1709,7 +1745,7 @@ int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int
   if (int rc = mailbox(&mb)) return rc;
   a.host_mail = mb->d;
   a.seq = ++mb->seq;
-  a.rev = fcn_flip(d_work, a.groups);
+  a.rev = fcn_flip(d_work, n * (int64_t)sizeof(double), a.groups);
   cudaStream_t st = as_stream(stream);
   if (variant == kFcnFast)
     k_nll_many<kFcnFast><<<chunk_grid(a.tiles * a.groups), kBlock, 0, st>>>(a);
