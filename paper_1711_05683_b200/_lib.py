@@ -251,6 +251,17 @@ def lib() -> ctypes.CDLL:
 
 
 _raw_stream = None
+_get_device = None
+
+
+def current_device() -> int:
+    """Index of the current CUDA device (torch's C-level query when it exists:
+    no Python wrapper layers on the FCN's per-call path)."""
+    global _get_device
+    if _get_device is None:
+        t = torch()
+        _get_device = getattr(t._C, "_cuda_getDevice", None) or t.cuda.current_device
+    return _get_device()
 
 
 def stream_ptr() -> int:
@@ -263,7 +274,7 @@ def stream_ptr() -> int:
         fn = getattr(t._C, "_cuda_getCurrentRawStream", None)
         _raw_stream = fn if fn is not None else False
     if _raw_stream:
-        return _raw_stream(t.cuda.current_device())
+        return _raw_stream(current_device())
     return t.cuda.current_stream().cuda_stream
 
 
