@@ -7,6 +7,8 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/prof
 bash tools/gpu_fp64.sh
+# the bench's FP64 rooflines read the DP counts of the kernels being measured
+python tools/fp64_roofline.py gpurun_out/dp_counts.csv gpurun_out/fp64_peak.jsonl r02 > /dev/null
 bash tools/gpu_evidence.sh
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
 bash tools/gpu_r02_ncu.sh > /dev/null
