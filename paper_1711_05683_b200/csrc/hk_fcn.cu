@@ -376,6 +376,9 @@ __global__ void __launch_bounds__(kBlock) k_nll(const double* __restrict__ x, in
 template <int V>
 __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const double* __restrict__ x, int64_t n,
                                                       const __grid_constant__ Coeffs c, FcnWork w) {
+#ifdef HK_PROBE_EMPTY  // timing probe: launch floor
+  return;
+#endif
   const int64_t chunks = w.full + w.tail_ctas;
   for (int64_t b = blockIdx.x; b < chunks; b += gridDim.x) {
     const int64_t ch = fcn_tile(w, b, chunks);
@@ -386,7 +389,9 @@ __global__ void __launch_bounds__(kBlock, HK_FCN_MIN_BLOCKS) k_nll_fused(const d
     if (bad) atomicMax(w.bad, bad);
     block_sum_store<1>(acc, w.part + ch);
   }
+#ifndef HK_PROBE_NOFINISH  // timing probe: no ticket, fold or publication
   fcn_finish(w, chunks, V == kFcnFast ? c.base : 0.0);
+#endif
 }
 
 // ----------------------------------------- TMA-pipelined kFcnFast FCN -----

@@ -116,9 +116,13 @@ __device__ __forceinline__ void fcn_range(const FcnWork& w, int64_t n, int64_t b
   *end = t0 + rem * (j + 1) / w.tail_ctas;
 }
 
-__device__ __forceinline__ void fcn_publish(const FcnWork& w, double total) {
-  const unsigned long long b = atomicExch(w.bad, 0ull);
-  const unsigned long long z = w.div0 ? atomicExch(w.div0, 0ull) : 0ull;
+// b, z: the first-bad and first-zero-divisor cells, read by the caller after
+// every CTA has finished (no other thread touches them any more), so they
+// are re-armed with plain stores
+__device__ __forceinline__ void fcn_publish(const FcnWork& w, double total, unsigned long long b,
+                                            unsigned long long z) {
+  if (b) *w.bad = 0ull;
+  if (z) *w.div0 = 0ull;
   w.out[0] = total;
   w.out[1] = __longlong_as_double((long long)~b);
   w.out[5] = __longlong_as_double((long long)~z);
@@ -131,6 +135,12 @@ __device__ __forceinline__ void fcn_publish(const FcnWork& w, double total) {
     __threadfence_system();
     w.host_mail[0] = w.seq;
   }
+}
+
+__device__ __forceinline__ void fcn_publish(const FcnWork& w, double total) {
+  const unsigned long long b = atomicExch(w.bad, 0ull);
+  const unsigned long long z = w.div0 ? atomicExch(w.div0, 0ull) : 0ull;
+  fcn_publish(w, total, b, z);
 }
 
 // Last CTA: fixed-order fold of the `chunks` tile partials, plus `base` (a
@@ -163,11 +173,17 @@ __device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks, dou
 #if !HK_FCN_ACQREL
   __threadfence();
 #endif
+  // the problem cells are final now: their loads overlap the partials' reads
+  unsigned long long b = 0ull, z = 0ull;
+  if (threadIdx.x == 0) {
+    b = __ldcg(w.bad);
+    if (w.div0) z = __ldcg(w.div0);
+  }
   double acc[1] = {0.0};
   for (int64_t i = threadIdx.x; i < chunks; i += kBlock) acc[0] += __ldcg(w.part + i);
   __shared__ double total;
   block_sum_store<1>(acc, &total);
-  if (threadIdx.x == 0) fcn_publish(w, total + base);
+  if (threadIdx.x == 0) fcn_publish(w, total + base, b, z);
 }
 
 // The FCN over a density functor dens(row, &div0) -> density (any model: the
