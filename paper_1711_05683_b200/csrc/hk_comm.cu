@@ -145,6 +145,7 @@ int32_t hk_clique_size(void) {
 }
 
 int hk_allreduce_partials(double* const* d_bufs, int32_t n_dev, int64_t count, void* const* streams) {
+  HK_NVTX("hk_allreduce_partials");
   std::lock_guard<std::mutex> lock(g_mu);
   if (int rc = check_clique(n_dev, count)) return rc;
   HK_REQUIRE(d_bufs, "NULL buffer list");
@@ -165,6 +166,7 @@ int hk_allreduce_partials(double* const* d_bufs, int32_t n_dev, int64_t count, v
 
 int hk_allgather_partials(const double* const* d_send, double* const* d_recv, int32_t n_dev,
                           int64_t count, void* const* streams) {
+  HK_NVTX("hk_allgather_partials");
   std::lock_guard<std::mutex> lock(g_mu);
   if (int rc = check_clique(n_dev, count)) return rc;
   HK_REQUIRE(d_send && d_recv, "NULL buffer list");

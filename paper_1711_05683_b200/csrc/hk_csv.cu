@@ -377,6 +377,7 @@ int64_t hk_csv_scratch_bytes(int64_t n_rows, int32_t n_cols) {
 
 int hk_format_csv(const double* const* d_cols, int32_t n_cols, int64_t n_rows, void* d_scratch,
                   char* d_out, int64_t out_cap, int64_t* h_len, void* stream) {
+  HK_NVTX("hk_format_csv");
   HK_REQUIRE(d_cols && n_cols >= 1 && n_cols <= 4 * HK_MAX_DAUGHTERS + 1, "bad columns (%d)", n_cols);
   HK_REQUIRE(n_rows >= 0 && h_len, "bad arguments");
   *h_len = 0;

@@ -1575,6 +1575,7 @@ int64_t hk_nll_work_doubles(int64_t n) {
 int hk_nll_program_eval(const double* const* d_obs, int64_t n, const hk_density_t* model,
                         double* d_work, double* h_logsum, uint64_t* h_first_bad,
                         uint64_t* h_first_div0, void* stream) {
+  HK_NVTX("hk_nll_program_eval");
   if (int rc = validate_density(model)) return rc;
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
   HK_REQUIRE(d_obs && d_work && (!h_logsum || h_first_bad), "NULL pointer");
@@ -1605,6 +1606,7 @@ int hk_nll_program_eval(const double* const* d_obs, int64_t n, const hk_density_
 
 int hk_nll_combine(const double* d_gathered, int32_t world, double* h_logsum, uint64_t* h_first_bad,
                    uint64_t* h_first_div0, void* stream) {
+  HK_NVTX("hk_nll_combine");
   HK_REQUIRE(world >= 1 && d_gathered && h_logsum && h_first_bad, "bad combine arguments");
   Mailbox* mb = nullptr;
   if (int rc = mailbox(&mb)) return rc;
@@ -1620,6 +1622,7 @@ int hk_nll_combine(const double* d_gathered, int32_t world, double* h_logsum, ui
 
 int hk_ratio_partials_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
                               double* d_partials, uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_ratio_partials_program");
   RatioArgs a;
   if (int rc = fill_ratio_args(d_obs, n, model, &a)) return rc;
   if (n == 0) return HK_OK;
@@ -1636,6 +1639,7 @@ int hk_ratio_partials_program(const double* const* d_obs, int64_t n, const hk_de
 int hk_splot_weights_program(const double* const* d_obs, int64_t n, const hk_density_t* model,
                              const double* V, double* const* d_out, uint64_t* d_first_bad,
                              void* stream) {
+  HK_NVTX("hk_splot_weights_program");
   SplotProgArgs a;
   std::memset(&a, 0, sizeof(a));
   if (int rc = fill_ratio_args(d_obs, n, model, &a.r)) return rc;
@@ -1656,6 +1660,7 @@ int hk_splot_weights_program(const double* const* d_obs, int64_t n, const hk_den
 
 int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                     uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_nll_partials");
   Coeffs c;
   if (int rc = make_coeffs(model, &c)) return rc;
   HK_REQUIRE(n >= 0, "negative n");
@@ -1667,6 +1672,7 @@ int hk_nll_partials(const double* d_x, int64_t n, const hk_model_t* model, doubl
 
 int hk_nll_eval(const double* d_x, int64_t n, const hk_model_t* model, double* d_work,
                 double* h_logsum, uint64_t* h_first_bad, void* stream) {
+  HK_NVTX("hk_nll_eval");
   Coeffs c;
   if (int rc = make_coeffs(model, &c, n)) return rc;
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
@@ -1703,6 +1709,7 @@ int64_t hk_nll_many_work_doubles(int64_t n, int32_t k) {
 
 int hk_nll_eval_many(const double* d_x, int64_t n, const hk_model_t* models, int32_t k, double* d_work,
                      double* h_logsums, uint64_t* h_first_bad, void* stream) {
+  HK_NVTX("hk_nll_eval_many");
   HK_REQUIRE(k >= 1 && k <= HK_MAX_POINTS, "point count %d outside 1..%d", k, HK_MAX_POINTS);
   HK_REQUIRE(n > 0, "cannot evaluate an empty data set");
   HK_REQUIRE(d_x && d_work && models && h_logsums && h_first_bad, "NULL pointer");
@@ -1818,6 +1825,7 @@ int hk_fcn_session_start(const double* d_x, int64_t n, double* d_work, int64_t i
 }
 
 int hk_fcn_session_eval(const hk_model_t* model, double* h_logsum, uint64_t* h_first_bad) {
+  HK_NVTX("hk_fcn_session_eval");
   Session& S = t_session;
   HK_REQUIRE(S.active, "no FCN session on this thread (hk_fcn_session_start)");
   HK_REQUIRE(h_logsum && h_first_bad, "NULL pointer");
@@ -1883,6 +1891,7 @@ int64_t hk_fcn_session_device_ns(void) {
 
 int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, double* d_partials,
                       uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_yield_partials");
   HK_REQUIRE(model && model->n_comp >= 1 && model->n_comp <= 4,
              "yield stationarity supports 1..4 components");
   PdfCoeffs c;
@@ -1904,6 +1913,7 @@ int hk_yield_partials(const double* d_x, int64_t n, const hk_model_t* model, dou
 
 int hk_splot_weights(const double* d_x, int64_t n, const hk_model_t* model, const double* V,
                      double* const* d_out, uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_splot_weights");
   HK_REQUIRE(model && model->n_comp >= 1 && model->n_comp <= 4, "sPlot supports 1..4 species");
   HK_REQUIRE(V && d_out, "NULL pointer");
   SplotArgs a;
@@ -1928,6 +1938,7 @@ int64_t hk_column_stats_work_doubles(int64_t n) {
 }
 
 int hk_column_stats(const double* d_x, int64_t n, double* d_work, double* h_out, void* stream) {
+  HK_NVTX("hk_column_stats");
   HK_REQUIRE(n > 0 && d_x && d_work && h_out, "bad column-statistics arguments");
   cudaStream_t st = as_stream(stream);
   const int64_t chunks = (n + kFcnTile - 1) / kFcnTile;
@@ -1942,6 +1953,7 @@ int hk_column_stats(const double* d_x, int64_t n, double* d_work, double* h_out,
 
 int hk_model_density(const double* d_x, int64_t n, const hk_model_t* model, double* d_out,
                      void* stream) {
+  HK_NVTX("hk_model_density");
   Coeffs c;
   if (int rc = make_coeffs(model, &c)) return rc;
   HK_REQUIRE(n >= 0, "negative n");

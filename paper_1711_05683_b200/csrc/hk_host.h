@@ -10,7 +10,21 @@
 
 #include "hepkit_cuda.h"
 
+// NVTX ranges (header-only NVTX v3: no link dependency; a no-op unless a
+// profiler injects its tool library): every compute entry point of the C ABI
+// opens one named after itself, so nsys / ncu --nvtx timelines show the
+// reference-facing calls around their kernels.
+#include <nvtx3/nvToolsExt.h>
+
 namespace hk {
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define HK_NVTX(name) ::hk::NvtxRange hk_nvtx_range_(name)
 
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* where);

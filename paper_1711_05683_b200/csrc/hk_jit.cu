@@ -482,6 +482,7 @@ int64_t hk_jit_source(const hk_program_t* f, int32_t n_daughters, int32_t rng_mo
 }
 
 int hk_jit_compile(const hk_program_t* f, int32_t n_daughters, int32_t rng_mode, int64_t* cubin_bytes) {
+  HK_NVTX("hk_jit_compile");
   HK_REQUIRE(f && f->n_ops >= 1 && f->n_ops <= HK_MAX_PROGRAM, "bad program");
   HK_REQUIRE(n_daughters == -1 || n_daughters == 0 || (n_daughters >= 2 && n_daughters <= 8),
              "n_daughters %d", n_daughters);

@@ -856,6 +856,7 @@ int64_t hk_num_chunks(int64_t ev_count) { return num_chunks(ev_count); }
 
 int hk_rng_raw64(const hk_key_t* key, const uint64_t* d_counters, int64_t n, uint64_t* d_out,
                  void* stream) {
+  HK_NVTX("hk_rng_raw64");
   if (int rc = validate_key(key, "hk_rng_raw64")) return rc;
   HK_REQUIRE(n >= 0, "negative n");
   if (n == 0) return HK_OK;
@@ -875,6 +876,7 @@ int hk_philox4x32_10(const uint32_t* d_ctr_key, int64_t n, uint32_t* d_out, void
 
 int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, double* d_out,
                    void* stream) {
+  HK_NVTX("hk_rng_uniform");
   if (int rc = validate_key(key, "hk_rng_uniform")) return rc;
   HK_REQUIRE(n >= 0, "negative n");
   if (n == 0) return HK_OK;
@@ -886,6 +888,7 @@ int hk_rng_uniform(const hk_key_t* key, const uint64_t* d_counters, int64_t n, d
 
 int hk_phsp_generate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
                      int64_t ev_count, double* const* d_cols, double* d_wpartials, void* stream) {
+  HK_NVTX("hk_phsp_generate");
   if (int rc = validate_decay(spec, "hk_phsp_generate")) return rc;
   if (int rc = validate_key(key, "hk_phsp_generate")) return rc;
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
@@ -917,6 +920,7 @@ int hk_phsp_decay_chain(const double* d_w_in, const double* const* d_p4_in,
                         const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
                         int64_t ev_count, double* d_w_out, double* const* d_sub_cols,
                         uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_phsp_decay_chain");
   if (int rc = validate_decay(sub, "hk_phsp_decay_chain")) return rc;
   if (int rc = validate_key(sub_key, "hk_phsp_decay_chain")) return rc;
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
@@ -981,6 +985,7 @@ int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t 
                            const hk_decay_t* sub, const hk_key_t* sub_key, uint64_t ev_begin,
                            int64_t ev_count, double* const* d_cols, double* d_wpartials,
                            uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_phsp_generate_chain");
   if (int rc = validate_decay(spec, "hk_phsp_generate_chain")) return rc;
   if (int rc = validate_decay(sub, "hk_phsp_generate_chain")) return rc;
   if (int rc = validate_key(key, "hk_phsp_generate_chain")) return rc;
@@ -1019,6 +1024,7 @@ int hk_phsp_generate_chain(const hk_decay_t* spec, const hk_key_t* key, int32_t 
 int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_count,
                     const hk_program_t* f, double* d_partials, uint64_t* d_first_bad,
                     void* stream) {
+  HK_NVTX("hk_phsp_moments");
   HK_REQUIRE(d_cols && n_cols >= 1 && n_cols <= kMaxCols, "bad columns (%d)", n_cols);
   if (int rc = validate_program(f, n_cols)) return rc;
   HK_REQUIRE(ev_count >= 0, "negative ev_count");
@@ -1052,6 +1058,7 @@ int hk_phsp_moments(const double* const* d_cols, int32_t n_cols, int64_t ev_coun
 
 int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const hk_program_t* f,
                    double* d_out, uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_map_program");
   HK_REQUIRE(d_cols && n_cols >= 1 && n_cols <= kMaxCols, "bad columns (%d)", n_cols);
   if (int rc = validate_program(f, n_cols)) return rc;
   HK_REQUIRE(n >= 0, "negative n");
@@ -1084,6 +1091,7 @@ int hk_map_program(const double* const* d_cols, int32_t n_cols, int64_t n, const
 int hk_phsp_integrate(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
                       int64_t ev_count, const hk_program_t* f, const hk_pair_integrand_t* pair,
                       double* d_partials, uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_phsp_integrate");
   if (int rc = validate_decay(spec, "hk_phsp_integrate")) return rc;
   if (int rc = validate_key(key, "hk_phsp_integrate")) return rc;
   const bool fast = pair && pair->kind != HK_PAIR_NONE;
@@ -1139,6 +1147,7 @@ int hk_fold_segments(const double* d_partials, int64_t n_segments, int32_t seg_l
 int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chunk_begin,
                    int64_t n_chunks_local, int32_t recs_per_chunk, int32_t width, int32_t s_begin,
                    int32_t s_count, double* d_out, void* stream) {
+  HK_NVTX("hk_fold_supers");
   HK_REQUIRE(width >= 1 && width <= kFoldMaxWidth && recs_per_chunk >= 1 && recs_per_chunk <= 1024,
              "bad record shape %d x %d", recs_per_chunk, width);
   HK_REQUIRE(n_chunks_total >= 0 && chunk_begin >= 0 && n_chunks_local >= 0 &&
@@ -1165,6 +1174,7 @@ int hk_fold_supers(const double* d_partials, int64_t n_chunks_total, int64_t chu
 
 int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, double* d_out,
                      void* stream) {
+  HK_NVTX("hk_fold_partials");
   HK_REQUIRE(width >= 1 && width <= kFoldMaxWidth, "fold width %d outside 1..%d", width, kFoldMaxWidth);
   HK_REQUIRE(n_parts >= 0 && d_out, "bad fold arguments");
   HK_REQUIRE(n_parts == 0 || d_partials, "NULL partials");
@@ -1174,6 +1184,7 @@ int hk_fold_partials(const double* d_partials, int64_t n_parts, int32_t width, d
 int hk_unweight_flags(const double* d_w, int64_t n, double w_max, const hk_key_t* key,
                       uint64_t ev_begin, uint8_t* d_flags, int64_t* d_counts,
                       uint64_t* d_first_bad, void* stream) {
+  HK_NVTX("hk_unweight_flags");
   if (int rc = validate_key(key, "hk_unweight_flags")) return rc;
   HK_REQUIRE(key->mode == HK_RNG_REFERENCE, "unweighting uses the reference stream");
   HK_REQUIRE(n >= 0, "negative n");
@@ -1204,6 +1215,7 @@ int hk_scan_counts(const int64_t* d_counts, int64_t n, int64_t* d_out, int64_t* 
 
 int hk_compact(const double* const* d_in, int32_t n_cols, int64_t n, const uint8_t* d_flags,
                const int64_t* d_offsets, double* const* d_out, int32_t weight_col, void* stream) {
+  HK_NVTX("hk_compact");
   HK_REQUIRE(n_cols >= 1 && n_cols <= kMaxCols, "bad column count %d", n_cols);
   HK_REQUIRE(n >= 0, "negative n");
   if (n == 0) return HK_OK;

@@ -107,6 +107,7 @@ int hk_device_info(int* n_devices, int* sm_count) {
 int hk_phsp_generate_host(const hk_decay_t* spec, const hk_key_t* key, uint64_t ev_begin,
                           int64_t ev_count, double* const* h_cols, double* h_wsums,
                           void* d_stage, size_t stage_bytes, void* stream) {
+  HK_NVTX("hk_phsp_generate_host");
   HK_REQUIRE(spec && key && h_cols && d_stage, "NULL argument");
   HK_REQUIRE(spec->n >= 2 && spec->n <= HK_MAX_DAUGHTERS, "bad daughter count %d", spec->n);
   HK_REQUIRE(ev_count >= 0, "negative ev_count");

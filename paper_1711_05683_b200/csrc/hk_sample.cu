@@ -71,6 +71,7 @@ extern "C" int hk_sample_pdf(const hk_program_t* f, int32_t dim, const double* l
                              const double* span, double ceiling, const hk_key_t* key,
                              uint64_t ev_begin, int64_t count, int32_t max_rounds,
                              double* const* d_out, uint64_t* d_bad, void* stream) {
+  HK_NVTX("hk_sample_pdf");
   HK_REQUIRE(f && lo && span && key && d_out && d_bad, "NULL argument");
   HK_REQUIRE(dim >= 1 && dim <= kMaxDim, "dimension %d outside 1..%d", dim, kMaxDim);
   HK_REQUIRE(key->mode == HK_RNG_REFERENCE, "sampling uses the reference stream");

@@ -1,0 +1,11 @@
+#!/bin/bash
+# generator occupancy A/B on both streams
+cd "$(dirname "$0")/.."
+for rep in 1 2; do
+for lib in default m3 m5 t64m8; do
+  for rng in reference philox; do
+    if [ "$lib" = default ]; then timeout 120 python tools/bench_gen.py --n 1e8 --reps 20 --rng $rng | sed "s/^{/{\"rng\": \"$rng\", /";
+    else HK_LIB_PATH=variants/$lib/libhepkit_cuda.so timeout 120 python tools/bench_gen.py --n 1e8 --reps 20 --rng $rng | sed "s/^{/{\"rng\": \"$rng\", /"; fi
+  done
+done
+done 2>&1 | tee gpurun_out/gen_occ_ab.jsonl
