@@ -508,7 +508,9 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
                   event store; 1024 super-chunk records cross GPUs
       C5_bw       the same with <BW_K*(892)(m^2_K pi)> (M=0.89555, G=0.0473)
       C5_generic  1e9 events of <m12^2 * BW(m12^2)>: the NVRTC-specialised
-                  kernel, the functor interpreter beside it"""
+                  kernel, the functor interpreter beside it
+      C4_generic  (1 GPU) FCN evals/s at 1e7 events for a Breit-Wigner +
+                  polynomial model of closures (the density-program path)"""
     from paper_1711_05683_b200.parallel import sharded_integrate
 
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
@@ -624,6 +626,54 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     with _lib.jit_mode(_lib.JIT_OFF):
         dt_int = _timed(torch, c5g, 1, dist)
     out["C5_generic"] = {"value": world * n5g / dt_jit, "interpreter": world * n5g / dt_int}
+    if world == 1:
+        out["C4_generic"] = fcn_generic(hk, torch)
+    return out
+
+
+def fcn_generic(hk, torch, n: int = FCN_EVENTS, evals: int = 200, keep: bool = False) -> dict:
+    """FCN evals/s at 1e7 events for a model outside the closed-form kernels:
+    a Breit-Wigner + linear polynomial of wrap_closure shapes (the reference's
+    nll accepts any Pdf shape, fitting.py:160-166), lowered once to a
+    parametric density program and run as an NVRTC-specialised kernel; the
+    parameters change every call (norms recomputed on the host)."""
+    import math
+
+    import numpy as np
+    P = hk.Parameter
+    lo, hi = 0.6, 1.2
+    m0, g, c0, c1 = P("m0", 0.8955), P("g", 0.0473), P("c0", 1.0), P("c1", 0.5)
+    bw = hk.wrap_closure(lambda x, p: 1.0 / ((x[0] - p["m0"].value) ** 2 + (0.5 * p["g"].value) ** 2), [m0, g])
+    poly = hk.wrap_closure(lambda x, p: p["c0"].value + p["c1"].value * x[0], [c0, c1])
+    region = hk.BoundedRegion(((lo, hi),))
+
+    def bw_norm(r):
+        h = 0.5 * g.value
+        return (math.atan((hi - m0.value) / h) - math.atan((lo - m0.value) / h)) / h
+
+    model = hk.add_pdfs([P("n_bw", 0.3 * n), P("n_poly", 0.7 * n)],
+                        [hk.make_pdf(bw, bw_norm, region),
+                         hk.make_pdf(poly, lambda r: c0.value * (hi - lo) + 0.5 * c1.value * (hi * hi - lo * lo),
+                                     region)])
+    x = np.random.default_rng(11).uniform(lo, hi, n)
+    data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+    points = [(0.8955, 0.0473), (0.8900, 0.0500)]
+
+    def one(i):
+        m0.set(points[i % 2][0]); g.set(points[i % 2][1])
+        return hk.nll(model, data, ["x0"])
+
+    for i in range(5):
+        one(i)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(evals):
+        one(i)
+    dt = (time.perf_counter() - t0) / evals
+    out = {"what": "FCN @1e7 events, Breit-Wigner + linear polynomial closures (NVRTC density program)",
+           "value": 1.0 / dt, "unit": "evals/s", "us_per_eval": dt * 1e6}
+    if keep:
+        out.update(_model=model, _data=data)
     return out
 
 

@@ -190,7 +190,12 @@ __device__ __forceinline__ void fcn_finish(const FcnWork& w, int64_t chunks, dou
 // interpreter or a specialised program).  Non-positive / non-finite densities
 // (fitting.py:200-205) and zero divisors (functors.py:200-207) are recorded
 // as ~row under atomicMax, so the smallest row wins and 0 means none.
-template <class Dens>
+// kUnroll (the NVRTC-specialised density): full tiles run their 16 rows
+// unrolled, so the compiler issues every row's column loads before the
+// arithmetic instead of one load latency per row; the rows, their order and
+// every rounding are those of the rolled loop (same values as the
+// interpreter's pass).
+template <bool kUnroll = false, class Dens>
 __device__ __forceinline__ void fcn_density_pass(const FcnWork& w, int64_t n, const Dens& dens) {
   const int64_t chunks = w.full + w.tail_ctas;
   for (int64_t b = blockIdx.x; b < chunks; b += gridDim.x) {
@@ -199,15 +204,21 @@ __device__ __forceinline__ void fcn_density_pass(const FcnWork& w, int64_t n, co
     fcn_range(w, n, ch, &begin, &end);
     unsigned long long bad = 0, zero = 0;
     LogProd lp;
+    const auto row = [&](int64_t r) {
+      bool z = false;
+      const double d = dens(r, z);
+      if (z) zero = max(zero, ~(unsigned long long)r);
+      if (!(d > 0.0) || !isfinite(d)) bad = max(bad, ~(unsigned long long)r);
+      lp.add(d);
+    };
+    if (kUnroll && end - begin == kFcnTile) {
+#pragma unroll
+      for (int i = 0; i < kFcnRows; ++i) row(begin + threadIdx.x + (int64_t)i * kBlock);
+    } else {
 #pragma unroll 1
-    for (int i = 0; i < kFcnRows; ++i) {
-      const int64_t r = begin + threadIdx.x + (int64_t)i * kBlock;
-      if (r < end) {
-        bool z = false;
-        const double d = dens(r, z);
-        if (z) zero = max(zero, ~(unsigned long long)r);
-        if (!(d > 0.0) || !isfinite(d)) bad = max(bad, ~(unsigned long long)r);
-        lp.add(d);
+      for (int i = 0; i < kFcnRows; ++i) {
+        const int64_t r = begin + threadIdx.x + (int64_t)i * kBlock;
+        if (r < end) row(r);
       }
     }
     double acc[1] = {lp.value()};

@@ -281,7 +281,7 @@ std::string full_source(const hk_program_t& P, int n, int mode) {
            "};\n"
            "extern \"C\" __global__ void __launch_bounds__(256)\n"
            "    hk_jit_nll(const __grid_constant__ hk::FcnProgArgs a) {\n"
-           "  hk::fcn_density_pass(a.w, a.n, HkDensity{a});\n"
+           "  hk::fcn_density_pass<true>(a.w, a.n, HkDensity{a});\n"
            "}\n";
   if (n == 0)
     return "#define HK_JIT_MAX_COLS " + std::to_string(kJitMaxCols) + "\n" + kStoredPrelude +

@@ -186,6 +186,94 @@ def trace_arg_builder(arg_builder, names: Sequence[str]) -> list:
 
 
 # ---------------------------------------------------------------------------
+# symbolic-parameter tracing (the FCN's per-call fast path, fitting.lower_density)
+#
+# A model is lowered once with every Parameter as an IR leaf ("pv", k) instead
+# of its current value; each later call only reads the parameters' values
+# into the program's constant slots.  Anything that needs a concrete
+# parameter value while tracing (math.* on it, float(), Python control flow)
+# raises NotImplementedError, and the caller falls back to tracing with the
+# current values on every call.
+
+class ParamTrace:
+    """Collects the parameters met while lowering with symbolic parameters,
+    and the value checks the builtin shapes would run (sigma > 0, tau != 0)."""
+
+    def __init__(self):
+        self.params: list[Parameter] = []
+        self.leaves: dict[int, tuple] = {}
+        self.checks: list[Callable[[], float]] = []
+
+    def leaf(self, p: Parameter) -> tuple:
+        node = self.leaves.get(id(p))
+        if node is None:
+            node = self.leaves[id(p)] = ("pv", len(self.params))
+            self.params.append(p)
+        return node
+
+
+_PTRACE: ParamTrace | None = None
+
+
+def _reads_only_args(fn) -> bool:
+    """True when a closure's code reads nothing but its arguments and global
+    modules (numpy): no captured cells, no other globals, no nested code.
+    Only such a closure is a pure function of (x, p), so it can be traced
+    once with symbolic parameters; anything else (a captured Parameter read
+    directly, a module-level constant the user may rebind) is re-traced at
+    the current values on every call."""
+    import dis
+    import types
+
+    code = getattr(fn, "__code__", None)
+    if code is None or code.co_freevars or code.co_cellvars:
+        return False
+    if any(isinstance(c, types.CodeType) for c in code.co_consts):
+        return False
+    glb = getattr(fn, "__globals__", {})
+    for ins in dis.get_instructions(code):
+        if ins.opname in ("LOAD_DEREF", "LOAD_CLASSDEREF", "LOAD_NAME", "STORE_GLOBAL", "LOAD_FROM_DICT_OR_DEREF"):
+            return False
+        if ins.opname == "LOAD_GLOBAL" and not isinstance(glb.get(ins.argval), types.ModuleType):
+            return False
+    return True
+
+
+class _SymParam:
+    """What a closure sees as p[name] while tracing with symbolic parameters."""
+
+    def __init__(self, param: Parameter, trace: ParamTrace):
+        self._param, self._trace = param, trace
+        self.name = param.name
+
+    @property
+    def value(self) -> "Sym":
+        return Sym(self._trace.leaf(self._param))
+
+
+class _SymParamSet:
+    def __init__(self, params: ParamSet, trace: ParamTrace):
+        self._params, self._trace = params, trace
+
+    def __getitem__(self, key):
+        return _SymParam(self._params[key], self._trace)
+
+    def __getattr__(self, name):
+        raise NotImplementedError(f"ParamSet.{name} while tracing with symbolic parameters")
+
+
+def lower_symbolic(fn: Callable[[], object]) -> tuple[object, ParamTrace]:
+    """Run fn() (which lowers expressions) with symbolic parameters."""
+    global _PTRACE
+    trace, prev = ParamTrace(), _PTRACE
+    _PTRACE = trace
+    try:
+        return fn(), trace
+    finally:
+        _PTRACE = prev
+
+
+# ---------------------------------------------------------------------------
 # expression classes
 
 class FunctorExpr:
@@ -250,6 +338,9 @@ class GaussianShape(FunctorExpr):
         return np.exp(-0.5 * z * z) / (s * _SQRT_2PI)
 
     def lower(self, args):
+        if _PTRACE is not None:
+            _PTRACE.checks.append(self._sigma)
+            return ("gauss", args[0], _PTRACE.leaf(self.mean), _PTRACE.leaf(self.sigma))
         return ("gauss", args[0], float(self.mean.value), float(self._sigma()))
 
     def _collect_params(self):
@@ -275,6 +366,9 @@ class ExponentialShape(FunctorExpr):
         return np.exp(-np.asarray(args[0], dtype=float) / t)
 
     def lower(self, args):
+        if _PTRACE is not None:
+            _PTRACE.checks.append(self._tau)
+            return ("expo", args[0], _PTRACE.leaf(self.tau))
         return ("expo", args[0], float(self._tau()))
 
     def _collect_params(self):
@@ -298,6 +392,8 @@ class BreitWigner(FunctorExpr):
         return 1.0 / ((np.asarray(args[0], dtype=float) - m0 * m0) ** 2 + (m0 * m0) * (g0 * g0))
 
     def lower(self, args):
+        if _PTRACE is not None:
+            return ("bw", args[0], _PTRACE.leaf(self.m0), _PTRACE.leaf(self.g0))
         return ("bw", args[0], float(self.m0.value), float(self.g0.value))
 
     def _collect_params(self):
@@ -330,8 +426,11 @@ class Closure(FunctorExpr):
         return self.fn(args, self.params)
 
     def lower(self, args):
+        if _PTRACE is not None and not _reads_only_args(self.fn):
+            raise NotImplementedError("closure reads state outside its arguments")
+        params = self.params if _PTRACE is None else _SymParamSet(self.params, _PTRACE)
         try:
-            out = self.fn(tuple(Sym(a) for a in args), self.params)
+            out = self.fn(tuple(Sym(a) for a in args), params)
         except NotImplementedError:
             raise
         except Exception as exc:  # noqa: BLE001
@@ -566,6 +665,12 @@ def compile_program(root, keep: Sequence = (), params: Sequence[float] | None = 
     return prog
 
 
+def _param_leaf(v):
+    """A builtin shape's parameter inside its op: a value, or (symbolic
+    parameter tracing) already an IR leaf."""
+    return v if isinstance(v, tuple) else ("const", v)
+
+
 def desugar(node):
     """Builtin shape ops (gauss/expo/bw, which carry their parameters inside
     the op) rewritten as primitive ops with constant leaves, in the
@@ -578,16 +683,16 @@ def desugar(node):
         if key in memo:
             return memo[key]
         kind = n[0]
-        if kind in ("col", "const"):
+        if kind in ("col", "const", "pv", "nv", "yv"):
             out = n
         elif kind == "gauss":
-            a, mu, s = walk(n[1]), ("const", n[2]), ("const", n[3])
+            a, mu, s = walk(n[1]), _param_leaf(n[2]), _param_leaf(n[3])
             z = ("udiv", ("sub", a, mu), s)
             out = ("udiv", ("exp", ("mul", ("mul", ("const", -0.5), z), z)), ("mul", s, ("const", _SQRT_2PI)))
         elif kind == "expo":
-            out = ("exp", ("udiv", ("neg", walk(n[1])), ("const", n[2])))
+            out = ("exp", ("udiv", ("neg", walk(n[1])), _param_leaf(n[2])))
         elif kind == "bw":
-            m0, g0 = ("const", n[2]), ("const", n[3])
+            m0, g0 = _param_leaf(n[2]), _param_leaf(n[3])
             m2 = ("mul", m0, m0)
             t = ("sub", walk(n[1]), m2)
             out = ("udiv", ("const", 1.0), ("add", ("mul", t, t), ("mul", m2, ("mul", g0, g0))))
@@ -615,6 +720,9 @@ def parametrize(roots: Sequence) -> tuple[tuple, list[float]]:
         if kind == "const":
             out = ("const", ("p", len(values)))
             values.append(float(n[1]))
+        elif kind in ("pv", "nv", "yv"):   # symbolic parameter / norm / yield: a slot, the leaf as its source
+            out = ("const", ("p", len(values)))
+            values.append(n)
         elif kind == "col":
             out = n
         else:

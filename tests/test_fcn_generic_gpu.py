@@ -349,3 +349,42 @@ def test_nll_regimes_vs_oracle(cuda, hk, mu, sigma, tau):
     assert abs(got - want) <= 1e-10 * abs(want)
     assert hk.nll(model, data, ["x0"]) == got
     assert nll_many(model, data, ["x0"], [model.param_set().values()] * 3) == [got] * 3
+
+
+_SCAN_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1711_05683_b200 as hk
+from paper_1711_05683_b200.fitting import nll_many
+rs = np.random.default_rng(21)
+x = np.clip(np.concatenate([rs.normal(5, 0.5, 400_000), rs.exponential(3.0, 600_123)]), 1e-3, 9.999)
+data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+P = hk.Parameter
+region = hk.BoundedRegion(((0.0, 10.0),))
+g = hk.shape_gaussian(P("mean", 5.0), P("sigma", 0.5))
+e = hk.shape_exponential(P("tau", 3.0))
+m = hk.add_pdfs([P("n_sig", 4e5), P("n_bkg", 6e5)],
+                [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+vals = [hk.nll(m, data, ["x0"]) for _ in range(3)] + nll_many(m, data, ["x0"], [m.param_set().values()] * 5)
+print(repr([float(v).hex() for v in vals]))
+"""
+
+
+def test_fcn_scan_direction_does_not_change_values(cuda):
+    """The FCN's tile scan order is an L2 hint (csrc/hk_fcn.cu fcn_flip): last
+    to first for columns within 0.85 of L2, alternating per call beyond
+    (HK_FCN_REV_MAX_BYTES=0 forces alternation here).  Every order gives the
+    same bits, single-point and batched."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _SCAN_SCRIPT.format(root=root)
+    outs = []
+    for thr in ("0", str(1 << 40)):
+        env = dict(os.environ, HK_FCN_REV_MAX_BYTES=thr)
+        r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(eval(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    assert len(set(outs[0])) == 1
