@@ -856,7 +856,7 @@ __device__ __forceinline__ void server_tiles(const ServerArgs& a, const FPoint& 
     __syncthreads();  // every thread has read s_tile
     unsigned long long nxt = 0;
     if (threadIdx.x == 0) nxt = atomicAdd(&a.dev->next, 1ull);
-    server_tile<V>(a, c, ch);
+    server_tile<V>(a, c, fcn_tile(a.w, ch, chunks));  // in the pass's scan direction (fcn_flip)
     if (threadIdx.x == 0) s_tile = (long long)nxt;
     __syncthreads();
     ch = s_tile;
