@@ -510,7 +510,9 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
       C5_generic  1e9 events of <m12^2 * BW(m12^2)>: the NVRTC-specialised
                   kernel, the functor interpreter beside it
       C4_generic  (1 GPU) FCN evals/s at 1e7 events for a Breit-Wigner +
-                  polynomial model of closures (the density-program path)"""
+                  polynomial model of closures (the density-program path)
+      UNWEIGHT    phsp_unweight of the stored 1e8 block (accept flags + compaction)
+      TOYS        (1 GPU) generate_model_sample of the C4 model, 1e7 events"""
     from paper_1711_05683_b200.parallel import sharded_integrate
 
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
@@ -577,6 +579,21 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     dt = _timed(torch, c2avg, 10, dist)
     out["C2_average"] = {"value": world * EVENTS_PER_GPU / dt, "ms": dt * 1e3,
                          "frac_copy": 72 * EVENTS_PER_GPU / dt / 1e9 / peak}
+    # UNWEIGHT: accept-reject of the stored 1e8 block against
+    # phsp_max_weight, order-preserving compaction of the accepted rows
+    w_max = hk.phsp_max_weight(spec)
+    acc = {}
+
+    def unw():
+        acc["b"] = hk.phsp_unweight(blk, w_max, hk.RngKey(1, 4), row_offset=rank * EVENTS_PER_GPU)
+
+    dt = _timed(torch, unw, 5, dist)
+    n_acc = len(acc.pop("b"))
+    # flags: 8 B weight read + 1 B flag written; compaction: 1 B flag + 13 columns read
+    # and written for each accepted row (flag scan and counts are negligible)
+    ub = 9 * EVENTS_PER_GPU + EVENTS_PER_GPU + 2 * 104 * n_acc
+    out["UNWEIGHT"] = {"value": world * EVENTS_PER_GPU / dt, "ms": dt * 1e3, "accepted": n_acc,
+                       "frac_copy": ub / dt / 1e9 / peak}
     # CSV: write_csv of 1e7 stored rows, GPU-formatted text streamed to a file
     from paper_1711_05683_b200.store import ColumnStore
     n_csv = 10_000_000
@@ -628,7 +645,32 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     out["C5_generic"] = {"value": world * n5g / dt_jit, "interpreter": world * n5g / dt_int}
     if world == 1:
         out["C4_generic"] = fcn_generic(hk, torch)
+        out["TOYS"] = toy_sample(hk, torch)
     return out
+
+
+def toy_sample(hk, torch) -> dict:
+    """the C4 data set itself -- generate_model_sample of
+    the benchmark model (build_model(scale=200): 4e6 Gaussian + 6e6
+    exponential events, RngKey(7, 2), poisson=False; fitting.py:526-552) by
+    device accept-reject, events/s (host wall clock around the API call)."""
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(P("mean", 5.0), P("sigma", 0.5))
+    e = hk.shape_exponential(P("tau", 3.0))
+    model = hk.add_pdfs([P("n_sig", 4e6), P("n_bkg", 6e6)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+    for _ in range(2):
+        data = hk.generate_model_sample(model, hk.RngKey(7, 2), poisson=False)
+    torch.cuda.synchronize()
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        data = hk.generate_model_sample(model, hk.RngKey(7, 2), poisson=False)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    return {"what": "generate_model_sample of the C4 model, 1e7 events (device accept-reject)",
+            "value": len(data) / dt, "ms": dt * 1e3}
 
 
 def fcn_generic(hk, torch, n: int = FCN_EVENTS, evals: int = 200, keep: bool = False) -> dict:

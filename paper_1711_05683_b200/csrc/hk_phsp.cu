@@ -543,32 +543,63 @@ struct CompactArgs {
   const long long* offsets;
 };
 
-// order-preserving compaction: thread t owns 16 consecutive rows of the chunk
+// Order-preserving compaction of one 4096-row chunk per CTA iteration, rows
+// walked in the kernels' usual 256-row stripes (row c*4096 + i*256 + t), so
+// every column load is a coalesced warp transaction and the accepted rows of
+// a stripe are stored to consecutive addresses.  A row's destination is the
+// chunk's offset + the accepted rows before it in (stripe, warp, lane)
+// order: warp ballots per stripe, one 128-entry exclusive scan per chunk.
 __global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ CompactArgs a) {
+  constexpr int kWarps = kBlock / 32;
   const int64_t chunks = (a.n + HK_CHUNK - 1) / HK_CHUNK;
-  __shared__ int sm[kBlock];
+  __shared__ int s_pre[kRowsPerThread * kWarps];  // (stripe, warp) counts, then their exclusive scan
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
-    const int64_t r0 = c * HK_CHUNK + (int64_t)threadIdx.x * kRowsPerThread;
-    unsigned mask = 0;
+    const int64_t c0 = c * HK_CHUNK + threadIdx.x;
+    unsigned bits = 0;
+#pragma unroll
     for (int i = 0; i < kRowsPerThread; ++i) {
-      const int64_t r = r0 + i;
-      if (r < a.n && a.flags[r]) mask |= 1u << i;
+      const int64_t r = c0 + i * kBlock;
+      const bool f = r < a.n && a.flags[r];
+      bits |= (unsigned)f << i;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_pre[i * kWarps + warp] = __popc(m);
     }
-    sm[threadIdx.x] = __popc(mask);
     __syncthreads();
-    for (int off = 1; off < kBlock; off <<= 1) {
-      int v = threadIdx.x >= (unsigned)off ? sm[threadIdx.x - off] : 0;
-      __syncthreads();
-      sm[threadIdx.x] += v;
-      __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 128 counts: 4 consecutive entries per lane
+      constexpr int kPer = kRowsPerThread * kWarps / 32;
+      int v[kPer], tot = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        v[k] = s_pre[lane * kPer + k];
+        tot += v[k];
+      }
+      int inc = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      int run = inc - tot;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        s_pre[lane * kPer + k] = run;
+        run += v[k];
+      }
     }
-    int64_t dst = a.offsets[c] + (threadIdx.x == 0 ? 0 : sm[threadIdx.x - 1]);
+    __syncthreads();
+    const int64_t base = a.offsets[c];
+#pragma unroll 1
     for (int i = 0; i < kRowsPerThread; ++i) {
-      if (!(mask & (1u << i))) continue;
-      const int64_t r = r0 + i;
-      for (int col = 0; col < a.n_cols; ++col)
-        a.out[col][dst] = col == a.weight_col ? 1.0 : a.in[col][r];
-      ++dst;
+      const bool f = (bits >> i) & 1u;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int64_t dst = base + s_pre[i * kWarps + warp] + __popc(m & lt);
+        const int64_t r = c0 + i * kBlock;
+        for (int col = 0; col < a.n_cols; ++col)
+          a.out[col][dst] = col == a.weight_col ? 1.0 : __ldcs(a.in[col] + r);
+      }
     }
     __syncthreads();
   }
