@@ -45,6 +45,7 @@ extern "C" {
 
 #define HK_CHUNK 4096        /* rows per reduction partial (parallel.py:18) */
 #define HK_WARP_SLICES 8     /* per-warp weight partials per chunk (generation kernels) */
+#define HK_SUPERS 1024       /* fixed super-chunks per run: the multi-GPU exchange grid (hk_fold_supers) */
 #define HK_MAX_DAUGHTERS 16  /* templated fast path covers n <= 8 */
 #define HK_MAX_PROGRAM 256   /* ops per device functor program */
 #define HK_MAX_SLOTS 32      /* virtual registers per program */

@@ -401,3 +401,20 @@ def test_chain_fixed_frame_mass_predicate(hk):
     massless = _lib.make_decay(hk.DecaySpec(2.0, (0.0, 0.5)))
     assert L.hk_chain_fixed_frame_mass(massless, 1, _lib.make_decay(hk.DecaySpec(0.3, (0.1, 0.1)))) == 0.0
     assert L.hk_chain_fixed_frame_mass(spec, 4, pion) == 0.0
+
+
+def test_python_constants_match_header(hk):
+    """Every integer #define of include/hepkit_cuda.h that _lib mirrors has
+    the header's value (sizes, limits, sentinels)."""
+    import os
+    import re
+    from paper_1711_05683_b200 import _lib
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "include", "hepkit_cuda.h")).read()
+    seen = 0
+    for name, value in re.findall(r"#define\s+(HK_\w+)\s+(0x[0-9A-Fa-f]+|\d+)\b", text):
+        if hasattr(_lib, name):
+            assert getattr(_lib, name) == int(value, 0), name
+            seen += 1
+    assert seen >= 8
+    assert _lib.HK_SUPERS == 1024
