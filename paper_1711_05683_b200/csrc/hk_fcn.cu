@@ -235,7 +235,10 @@ __device__ __forceinline__ void fast_row(const C& c, double x, double& prod) {
 }
 
 // column loads of the kFcnFast tiles (HK_FCN_LD: 0 __ldg; 1 ld.global.nc
-// with an L2 evict_last policy; 2 plain ld.global with evict_last)
+// with an L2 evict_last policy; 2 plain ld.global with evict_last).  The
+// evict_last policies measured no gain on B200 (1e7: 20.4 vs 20.3 us; the
+// scan order is what keeps the column in L2, fcn_flip):
+// profiles/r02_fcn_ld_ab.jsonl, r02_fcn_l2_steady_state.txt
 #ifndef HK_FCN_LD
 #define HK_FCN_LD 0
 #endif
