@@ -94,10 +94,17 @@ std::string hex_const(double v) {
 // weight w, c = 1 + 4 j + k is p[4 j + k]).  Zero divisors set d0.
 // params: constants come from the kernel arguments (a.prog.cst[i]) instead of
 // being baked in -- the FCN module, compiled once per op structure.
+// params (the FCN module): constants are kernel arguments, and an unchecked
+// division by a value computed from constants only (a p.d.f. norm, a shape's
+// sigma) becomes a product with its reciprocal -- loop-invariant, so the
+// compiler computes it once per thread.  Each such quotient moves by <= 1
+// ulp, far inside the FCN's 1e-10 budget; the value an error message quotes
+// comes from the map module, which keeps every division exact.
 std::string emit_body(const hk_program_t& P, bool fused, bool params = false) {
   std::string s;
   int slot_of[HK_MAX_SLOTS];
   for (int& x : slot_of) x = -1;
+  bool cst_only[HK_MAX_PROGRAM] = {};
   auto v = [&](int slot) -> std::string {
     return slot_of[slot] < 0 ? std::string("0.0") : "v" + std::to_string(slot_of[slot]);
   };
@@ -140,9 +147,20 @@ std::string emit_body(const hk_program_t& P, bool fused, bool params = false) {
         break;
       case HK_OP_ADD0: e = "__dadd_rn(" + A + ", 0.0)"; break;
       case HK_OP_SQUARE: e = "__dmul_rn(" + A + ", " + A + ")"; break;
-      case HK_OP_UDIV: e = "__ddiv_rn(" + A + ", " + B + ")"; break;
+      case HK_OP_UDIV:
+        if (params && slot_of[P.b[i]] >= 0 && cst_only[slot_of[P.b[i]]])
+          e = "__dmul_rn(" + A + ", __drcp_rn(" + B + "))";
+        else
+          e = "__ddiv_rn(" + A + ", " + B + ")";
+        break;
       default: e = "__longlong_as_double(0x7ff8000000000000ll)"; break;
     }
+    const bool binary = P.op[i] == HK_OP_ADD || P.op[i] == HK_OP_SUB || P.op[i] == HK_OP_MUL ||
+                        P.op[i] == HK_OP_UDIV;
+    const bool unary = P.op[i] == HK_OP_NEG || P.op[i] == HK_OP_SQUARE || P.op[i] == HK_OP_ADD0;
+    const auto konst = [&](int slot) { return slot_of[slot] >= 0 && cst_only[slot_of[slot]]; };
+    cst_only[i] = P.op[i] == HK_OP_CONST || (binary && konst(P.a[i]) && konst(P.b[i])) ||
+                  (unary && konst(P.a[i]));
     s += "  const double v" + std::to_string(i) + " = " + e + ";\n";
     slot_of[P.dst[i]] = i;
   }
