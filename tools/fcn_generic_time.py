@@ -31,4 +31,18 @@ for _ in range(200):
 e1.record()
 e1.synchronize()
 out["kernel_us"] = e0.elapsed_time(e1) / 200 * 1e3
+import ctypes  # noqa: E402
+import time  # noqa: E402
+ls, fb, fz = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+for _ in range(10):
+    L.hk_nll_program_eval(obs, n, dm, work.data_ptr(), ctypes.byref(ls), ctypes.byref(fb), ctypes.byref(fz), st)
+t0 = time.perf_counter()
+for _ in range(200):
+    L.hk_nll_program_eval(obs, n, dm, work.data_ptr(), ctypes.byref(ls), ctypes.byref(fb), ctypes.byref(fz), st)
+out["c_abi_us"] = (time.perf_counter() - t0) / 200 * 1e6
+from paper_1711_05683_b200.fitting import lower_density as _ld  # noqa: E402
+t0 = time.perf_counter()
+for _ in range(2000):
+    _ld(model)
+out["lower_density_us"] = (time.perf_counter() - t0) / 2000 * 1e6
 print(json.dumps(out))
