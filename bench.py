@@ -269,9 +269,42 @@ def cpu_reference(reps: int = 3) -> dict:
                 w = np.asarray(blk.column("weight"))
                 return float(np.sum(w)), float(np.sum(w * w))
             rp[f"workers_{workers}"] = 1_000_000 / _best_of(run, reps)
+    if ref is not None:
+        rp["fcn_1e7"] = reference_fcn(ref, cores, reps)
     out["reference_python"] = rp if rp else "baseline/_ref not installed on this box"
     out["sample"] = (f"C2 rate: port {n_port} events at {cores} threads and 5e6 at 1 thread; reference Python "
-                     f"1e6 events at workers=1 and {cores}; best of {reps}")
+                     f"1e6 events at workers=1 and {cores}; reference FCN at 1e7 events; best of {reps}")
+    return out
+
+
+def reference_fcn(ref, cores: int, reps: int) -> dict:
+    """The reference's own FCN (hepkit.nll, fitting.py:175-210) on this box's
+    host cores at the C4 size: the benchmark model (4e6 Gaussian + 6e6
+    exponential on [0, 10]) over 1e7 events, parameters alternating as in our
+    arm's loop (norms recomputed), best of `reps` at workers=1 and all cores."""
+    import numpy as np
+    P = ref.Parameter
+    region = ref.BoundedRegion(((0.0, 10.0),))
+    mean, sigma, tau = P("mean", 5.0), P("sigma", 0.5), P("tau", 3.0)
+    g = ref.shape_gaussian(mean, sigma)
+    e = ref.shape_exponential(tau)
+    model = ref.add_pdfs([P("n_sig", 4e6), P("n_bkg", 6e6)],
+                         [ref.make_pdf(g, ref.gaussian_norm(g), region),
+                          ref.make_pdf(e, ref.exponential_norm(e), region)])
+    rs = np.random.default_rng(7)
+    x = np.clip(np.concatenate([rs.normal(5.0, 0.5, 4_000_000), rs.exponential(3.0, 6_000_000)]), 1e-3, 9.999)
+    store = ref.ColumnStore.from_columns(ref.ColumnSchema.real64("x0"), [x])
+    out = {"events": len(x), "unit": "evals/s"}
+    k = [0]
+
+    def one(workers):
+        p = ((5.0, 0.5, 3.0), (4.9, 0.55, 2.8))[k[0] % 2]
+        k[0] += 1
+        mean.set(p[0]); sigma.set(p[1]); tau.set(p[2])
+        return ref.nll(model, store, ["x0"], workers=workers)
+
+    for workers in (1, cores):
+        out[f"workers_{workers}"] = 1.0 / _best_of(lambda w=workers: one(w), reps)
     return out
 
 
