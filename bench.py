@@ -271,9 +271,42 @@ def cpu_reference(reps: int = 3) -> dict:
             rp[f"workers_{workers}"] = 1_000_000 / _best_of(run, reps)
     if ref is not None:
         rp["fcn_1e7"] = reference_fcn(ref, cores, reps)
+        rp.update(reference_configs(ref, cores, reps))
     out["reference_python"] = rp if rp else "baseline/_ref not installed on this box"
     out["sample"] = (f"C2 rate: port {n_port} events at {cores} threads and 5e6 at 1 thread; reference Python "
                      f"1e6 events at workers=1 and {cores}; reference FCN at 1e7 events; best of {reps}")
+    return out
+
+
+def reference_configs(ref, cores: int, reps: int) -> dict:
+    """The reference's own Python on the other BASELINE configs (SURVEY
+    8(d) CPU baseline), rates in events/s at workers=1 and all cores, best of
+    `reps`: C1 (1e5 events per phsp_generate call), C3 (phsp_generate +
+    phsp_decay_chain J/psi -> mu mu, 1e6 events), C5 (phsp_average of m12^2
+    over a stored 1e6-event block)."""
+    spec, mother = ref.DecaySpec(M_B0, DAUGHTERS), ref.FourVector.at_rest(M_B0)
+    sub = ref.DecaySpec(3.0969, (0.1056583755, 0.1056583755))
+    blk = ref.phsp_generate(spec, mother, 1_000_000, ref.RngKey(1, 1))
+
+    def m12(cols):
+        e = cols["p1_e"] + cols["p2_e"]
+        px = cols["p1_px"] + cols["p2_px"]
+        py = cols["p1_py"] + cols["p2_py"]
+        pz = cols["p1_pz"] + cols["p2_pz"]
+        return (e * e - px * px - py * py - pz * pz,)
+
+    runs = {
+        "C1": (100_000, lambda w: ref.phsp_generate(spec, mother, 100_000, ref.RngKey(1, 1), workers=w)),
+        "C3": (1_000_000, lambda w: ref.phsp_decay_chain(
+            ref.phsp_generate(spec, mother, 1_000_000, ref.RngKey(1, 1), workers=w), 1, sub, ref.RngKey(2, 1),
+            workers=w)),
+        "C5": (1_000_000, lambda w: ref.phsp_average(ref.identity(), blk, m12, workers=w)),
+    }
+    out = {}
+    for name, (n, fn) in runs.items():
+        out[name] = {"events": n, "unit": "events/s"}
+        for workers in (1, cores):
+            out[name][f"workers_{workers}"] = n / _best_of(lambda w=workers, f=fn: f(w), reps)
     return out
 
 
