@@ -348,3 +348,47 @@ def test_cli_bench_sequence_on_the_drop_in(cuda, hk):
     assert len(sample) == 100_000
     values = {w: hk.nll(model, sample, ["x0"], workers=w) for w in (1, 2, 4, 8)}
     assert len(set(values.values())) == 1
+
+
+# --- TestUnweight / TestAverage / TestMaxWeight: the remaining contracts --------
+def test_unweight_two_body_accepts_all_and_names_a_violation(cuda, hk):
+    """A 2-body decay's weight is its maximum (acceptance one); a ceiling below
+    the block's largest weight raises the reference's "exceeds w_max"."""
+    spec = hk.DecaySpec(1.0, (0.2, 0.25))
+    blk = hk.phsp_generate(spec, hk.FourVector.at_rest(1.0), 5000, hk.RngKey(11, 1))
+    assert len(hk.phsp_unweight(blk, hk.phsp_max_weight(spec), hk.RngKey(11, 4))) == len(blk)
+    spec3 = hk.DecaySpec(1.0, (0.1, 0.1, 0.1))
+    three = hk.phsp_generate(spec3, hk.FourVector.at_rest(1.0), 1000, hk.RngKey(12, 1))
+    with pytest.raises(ValueError, match="exceeds w_max"):
+        hk.phsp_unweight(three, float(np.max(three.column("weight"))) * 0.5, hk.RngKey(12, 4))
+
+
+def test_average_of_one_and_the_empty_block(cuda, hk):
+    blk = hk.phsp_generate(hk.DecaySpec(1.0, (0.1, 0.1, 0.1)), hk.FourVector.at_rest(1.0), 1000,
+                           hk.RngKey(22, 1))
+    r = hk.phsp_average(hk.constant(1.0), blk, lambda cols: (cols["weight"] * 0 + 1,))
+    assert abs(r.value - 1.0) <= 1e-12 and abs(r.error) <= 1e-12
+    with pytest.raises(ValueError, match="empty"):
+        hk.phsp_average(hk.identity(), hk.ColumnStore(hk.phsp_schema(2)), lambda cols: (cols["weight"],))
+
+
+def test_max_weight_two_body_and_threshold(cuda, hk):
+    assert hk.phsp_max_weight(hk.DecaySpec(1.0, (0.3, 0.2))) == pytest.approx(
+        hk.breakup_momentum(1.0, 0.3, 0.2), rel=1e-15)
+    with pytest.raises(hk.BelowThreshold):
+        hk.phsp_max_weight(hk.DecaySpec(1.0, (0.6, 0.5)))
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4097, 300_001])
+@pytest.mark.parametrize("density", [0.0, 0.01, 0.5, 1.0])
+def test_device_selection_equals_numpy(cuda, hk, n, density):
+    """where_mask of a device store (the order-preserving compaction kernel
+    behind phsp_unweight) equals numpy boolean indexing, column by column."""
+    rs = np.random.default_rng(n + int(density * 100))
+    blk = hk.phsp_generate(hk.DecaySpec(1.0, (0.1, 0.1, 0.1)), hk.FourVector.at_rest(1.0), n,
+                           hk.RngKey(5, 1))
+    mask = rs.random(n) < density
+    sel = blk.where_mask(mask)
+    assert len(sel) == int(mask.sum())
+    for name in blk.schema.names:
+        assert np.array_equal(np.asarray(sel.column(name)), np.asarray(blk.column(name))[mask])
