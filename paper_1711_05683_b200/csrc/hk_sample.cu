@@ -3,9 +3,10 @@
 // proposal lo + u * span rounds exactly like the reference's numpy.
 //
 // Event j owns the counter block (j + key.counter) * 2^16: proposal round t
-// consumes counters +t*(d+1) .. +t*(d+1)+d (rng.py:214-219).  One thread per
-// event walks its rounds until acceptance, so the output is independent of
-// the launch shape, like the reference's worker invariance.
+// consumes counters +t*(d+1) .. +t*(d+1)+d (rng.py:214-219).  A thread walks
+// an event's rounds until acceptance, then takes the next event (k_sample),
+// so the output is independent of the launch shape, like the reference's
+// worker invariance.
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -33,34 +34,90 @@ struct SampleArgs {
   int64_t count;
   double* out[kMaxDim];
   unsigned long long* bad;  // [0] packed (batch, round, row) of a ceiling violation, [1] exhausted row
+  unsigned long long* next;  // work-stealing event counter (zeroed before the launch)
 };
 
-__global__ void __launch_bounds__(kBlock) k_sample(const __grid_constant__ SampleArgs a) {
-  const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-  if (i >= a.count) return;
-  const uint64_t ev = a.ev_begin + (uint64_t)i;
-  const uint64_t block0 = (ev + a.kc) * kProposalBlock;
+// One proposal round of event `ev`: returns 1 accepted (point stored), 2 a
+// ceiling violation (recorded), 0 rejected.
+__device__ __forceinline__ int sample_round(const SampleArgs& a, uint64_t ev, int64_t i, int t) {
   const int d = a.dim;
+  const uint64_t c0 = (ev + a.kc) * kProposalBlock + (uint64_t)t * (uint64_t)(d + 1);
   double pts[kMaxDim];
-  for (int t = 0; t < a.max_rounds; ++t) {
-    const uint64_t c0 = block0 + (uint64_t)t * (uint64_t)(d + 1);
-    for (int k = 0; k < d; ++k)
-      pts[k] = a.lo[k] + to_unit(mix64(a.base + (c0 + k) * kGolden) >> 11) * a.span[k];
-    const double u = to_unit(mix64(a.base + (c0 + d) * kGolden) >> 11);
-    bool div0 = false;
-    const double v = run_program(a.f, [&](int col) { return pts[col]; }, &div0);
-    if (v > a.ceiling) {
-      const unsigned long long key =
-          ((unsigned long long)(ev / kBatch) << 40) | ((unsigned long long)t << 24) | (ev % kBatch);
-      atomicMin(&a.bad[0], key);
-      return;
+  for (int k = 0; k < d; ++k) pts[k] = a.lo[k] + to_unit(mix64(a.base + (c0 + k) * kGolden) >> 11) * a.span[k];
+  const double u = to_unit(mix64(a.base + (c0 + d) * kGolden) >> 11);
+  bool div0 = false;
+  const double v = run_program(a.f, [&](int col) { return pts[col]; }, &div0);
+  if (v > a.ceiling) {
+    const unsigned long long key =
+        ((unsigned long long)(ev / kBatch) << 40) | ((unsigned long long)t << 24) | (ev % kBatch);
+    atomicMin(&a.bad[0], key);
+    return 2;
+  }
+  if (u * a.ceiling < v) {
+    for (int k = 0; k < d; ++k) a.out[k][i] = pts[k];
+    return 1;
+  }
+  return 0;
+}
+
+// Persistent threads with work stealing: a thread runs proposal rounds of its
+// current event and, once the event is accepted (or fails), takes the next
+// event index from a device counter (one atomic per warp for all the lanes
+// that need work).  With acceptance rate r a lane needs ~1/r rounds, but a
+// warp of one-event-per-thread lanes waits for its slowest lane (~3-4x the
+// mean at r = 1/8); here lanes stay busy until the events run out.  Each
+// event's point depends only on its own counters, so the output is the same
+// as one thread per event, whatever the schedule.
+__global__ void __launch_bounds__(kBlock) k_sample(const __grid_constant__ SampleArgs a) {
+  const int lane = threadIdx.x & 31;
+  int64_t i = -1;  // current event (row of the output), -1: needs one
+  int t = 0;
+  for (;;) {
+    const bool need = i < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      unsigned long long base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(a.next, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (need) {
+        i = (int64_t)(base + __popc(m & ((1u << lane) - 1u)));
+        t = 0;
+      }
     }
-    if (u * a.ceiling < v) {
-      for (int k = 0; k < d; ++k) a.out[k][i] = pts[k];
-      return;
+    const bool live = i < a.count;
+    if (!__any_sync(0xffffffffu, live)) break;
+    if (live) {
+      const uint64_t ev = a.ev_begin + (uint64_t)i;
+      const int r = sample_round(a, ev, i, t);
+      if (r != 0) {
+        i = -1;
+      } else if (++t == a.max_rounds) {
+        atomicMin(&a.bad[1], (unsigned long long)ev);
+        i = -1;
+      }
     }
   }
-  atomicMin(&a.bad[1], (unsigned long long)ev);
+}
+
+// the sampler's event counter on each device (zeroed before every launch)
+unsigned long long* sample_counter() {
+  static unsigned long long* ctr[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (!ctr[dev & 15] && cudaMalloc(&ctr[dev & 15], sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  return ctr[dev & 15];
+}
+
+int sample_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample, kBlock, 0);
+    grid = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+  }
+  return grid;
 }
 
 }  // namespace hk
@@ -95,6 +152,12 @@ extern "C" int hk_sample_pdf(const hk_program_t* f, int32_t dim, const double* l
   a.ev_begin = ev_begin;
   a.count = count;
   a.bad = reinterpret_cast<unsigned long long*>(d_bad);
-  k_sample<<<(unsigned)((count + kBlock - 1) / kBlock), kBlock, 0, as_stream(stream)>>>(a);
+  a.next = sample_counter();
+  HK_REQUIRE(a.next, "sampler counter allocation failed");
+  cudaStream_t st = as_stream(stream);
+  HK_CUDA(cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), st));
+  const int64_t want = (count + kBlock - 1) / kBlock;
+  const int g = sample_grid();
+  k_sample<<<(unsigned)(want < g ? want : g), kBlock, 0, st>>>(a);
   return check_launch("k_sample");
 }
