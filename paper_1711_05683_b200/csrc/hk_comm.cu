@@ -23,6 +23,7 @@ namespace hk {
 
 void jit_release();        // hk_jit.cu
 void fcn_release();        // hk_fcn.cu
+void sample_release();     // hk_sample.cu
 void copy_lane_release();  // hk_runtime.cu
 
 namespace {
@@ -135,6 +136,7 @@ int hk_shutdown(void) {
   }
   jit_release();
   fcn_release();
+  sample_release();
   copy_lane_release();
   return HK_OK;
 }

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "hepkit_cuda.h"
 #include "hk_device.cuh"
@@ -99,13 +101,26 @@ __global__ void __launch_bounds__(kBlock) k_sample(const __grid_constant__ Sampl
   }
 }
 
-// the sampler's event counter on each device (zeroed before every launch)
-unsigned long long* sample_counter() {
-  static unsigned long long* ctr[16] = {};
+// The sampler's event counter, one per (device, stream): calls on one stream
+// are serialised, calls on different streams get different counters.
+// Zeroed on the stream before every launch; freed by hk_shutdown.
+std::mutex g_ctr_mu;
+std::map<std::pair<int, cudaStream_t>, unsigned long long*> g_ctr;
+
+unsigned long long* sample_counter(cudaStream_t st) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  if (!ctr[dev & 15] && cudaMalloc(&ctr[dev & 15], sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-  return ctr[dev & 15];
+  std::lock_guard<std::mutex> lock(g_ctr_mu);
+  unsigned long long*& p = g_ctr[{dev, st}];
+  if (!p && cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) p = nullptr;
+  return p;
+}
+
+void sample_release() {
+  std::lock_guard<std::mutex> lock(g_ctr_mu);
+  for (auto& kv : g_ctr)
+    if (kv.second) cudaFree(kv.second);
+  g_ctr.clear();
 }
 
 int sample_grid() {
@@ -152,9 +167,9 @@ extern "C" int hk_sample_pdf(const hk_program_t* f, int32_t dim, const double* l
   a.ev_begin = ev_begin;
   a.count = count;
   a.bad = reinterpret_cast<unsigned long long*>(d_bad);
-  a.next = sample_counter();
-  HK_REQUIRE(a.next, "sampler counter allocation failed");
   cudaStream_t st = as_stream(stream);
+  a.next = sample_counter(st);
+  HK_REQUIRE(a.next, "sampler counter allocation failed");
   HK_CUDA(cudaMemsetAsync(a.next, 0, sizeof(unsigned long long), st));
   const int64_t want = (count + kBlock - 1) / kBlock;
   const int g = sample_grid();

@@ -55,3 +55,23 @@ def test_reductions_are_bitwise_repeatable(cuda, hk):
         else:
             for name, a, b in zip(("weights", "average", "fused", "interpreter", "fcn", "csv"), seen, got):
                 assert a == b, f"{name} differs between identical runs"
+
+
+def test_sampler_streams_are_independent(hk, cuda):
+    """The work-stealing sampler keeps one event counter per (device, stream):
+    two samples enqueued on two streams at once equal the same samples taken
+    one after the other."""
+    import numpy as np
+    torch = cuda
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(hk.Parameter("m", 5.0), hk.Parameter("s", 0.5))
+    want = [np.asarray(hk.sample_pdf(g, region, 400_000, hk.RngKey(k, 2), ceiling=1.0).column("x0"))
+            for k in (1, 2)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        a = hk.sample_pdf(g, region, 400_000, hk.RngKey(1, 2), ceiling=1.0)
+    with torch.cuda.stream(s2):
+        b = hk.sample_pdf(g, region, 400_000, hk.RngKey(2, 2), ceiling=1.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(np.asarray(a.column("x0")), want[0])
+    assert np.array_equal(np.asarray(b.column("x0")), want[1])
