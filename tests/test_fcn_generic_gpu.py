@@ -388,3 +388,53 @@ def test_fcn_scan_direction_does_not_change_values(cuda):
         outs.append(eval(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
     assert len(set(outs[0])) == 1
+
+
+def test_nll_random_models_vs_oracle(cuda, hk):
+    """Randomised Gaussian + exponential models and data shapes against the
+    oracle: whichever kernel the host proof (fast_coeffs) picks, the value
+    matches at 1e-10, and a non-positive density raises the reference's
+    message for the same event."""
+    from oracle import oracle as O  # checker only
+    rs = np.random.default_rng(2024)
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    import os
+    checked = raised = 0
+    cases = int(os.environ.get("HK_TEST_RANDOM_CASES", "40"))
+    for case in range(cases):
+        n = int(rs.integers(1, 200_000))
+        kind = case % 3
+        if kind == 0:
+            x = rs.uniform(0.0, 10.0, n)
+        elif kind == 1:
+            x = np.clip(rs.normal(rs.uniform(0, 10), rs.uniform(0.05, 3), n), 1e-6, 10.0)
+        else:
+            x = np.clip(rs.exponential(rs.uniform(0.2, 20), n), 0.0, 10.0)
+        mu, sigma = rs.uniform(-5, 15), 10 ** rs.uniform(-2, 0.7)
+        tau = (10 ** rs.uniform(-1.3, 1.7)) * (1 if rs.random() < 0.85 else -1)
+        n_sig, n_bkg = 10 ** rs.uniform(0, 6), 10 ** rs.uniform(0, 6)
+        g = hk.shape_gaussian(P("mean", mu), P("sigma", sigma))
+        e = hk.shape_exponential(P("tau", tau))
+        model = hk.add_pdfs([P("n_sig", n_sig), P("n_bkg", n_bkg)],
+                            [hk.make_pdf(g, hk.gaussian_norm(g), region),
+                             hk.make_pdf(e, hk.exponential_norm(e), region)])
+        data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+        norms = (O.gaussian_norm(mu, sigma, 0.0, 10.0), O.exponential_norm(tau, 0.0, 10.0))
+        if not all(np.isfinite(v) and v > 0 for v in norms):
+            # Pdf.norm's check comes first, as in the reference (fitting.py:80-89)
+            with pytest.raises(ValueError, match="normalization must be positive and finite"):
+                hk.nll(model, data, ["x0"])
+            continue
+        try:
+            want = O.nll(x, O.gauss_exp_components(mu, sigma, tau, n_sig, n_bkg))
+        except ValueError as exc:
+            with pytest.raises(ValueError) as got:
+                hk.nll(model, data, ["x0"])
+            assert str(got.value) == str(exc)
+            raised += 1
+            continue
+        got = hk.nll(model, data, ["x0"])
+        assert abs(got - want) <= 1e-10 * max(abs(want), 1.0), (case, mu, sigma, tau, got, want)
+        checked += 1
+    assert checked >= cases // 2
