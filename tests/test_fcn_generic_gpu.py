@@ -438,3 +438,44 @@ def test_nll_random_models_vs_oracle(cuda, hk):
         assert abs(got - want) <= 1e-10 * max(abs(want), 1.0), (case, mu, sigma, tau, got, want)
         checked += 1
     assert checked >= cases // 2
+
+
+def test_nll_random_closure_models_vs_numpy(cuda, hk):
+    """Randomised Breit-Wigner + polynomial closure models (the density-program
+    path, lowered once with symbolic parameters) against the reference
+    semantics evaluated with numpy on the same closures, at 1e-10, through
+    the interpreter and the NVRTC module alternately."""
+    import math
+    import os
+    from paper_1711_05683_b200 import _lib
+    rs = np.random.default_rng(77)
+    P = hk.Parameter
+    lo, hi = 0.6, 1.2
+    cases = int(os.environ.get("HK_TEST_RANDOM_CASES", "30"))
+    m0, g, c0, c1 = P("m0", 0.9), P("g", 0.05), P("c0", 1.0), P("c1", 0.5)
+    bw = hk.wrap_closure(lambda x, p: 1.0 / ((x[0] - p["m0"].value) ** 2 + (0.5 * p["g"].value) ** 2), [m0, g])
+    poly = hk.wrap_closure(lambda x, p: p["c0"].value + p["c1"].value * x[0], [c0, c1])
+    region = hk.BoundedRegion(((lo, hi),))
+
+    def bw_norm(r):
+        h = 0.5 * g.value
+        return (math.atan((hi - m0.value) / h) - math.atan((lo - m0.value) / h)) / h
+
+    def poly_norm(r):
+        return c0.value * (hi - lo) + 0.5 * c1.value * (hi * hi - lo * lo)
+
+    n_bw, n_poly = P("n_bw", 1.0), P("n_poly", 1.0)
+    model = hk.add_pdfs([n_bw, n_poly], [hk.make_pdf(bw, bw_norm, region), hk.make_pdf(poly, poly_norm, region)])
+    for case in range(cases):
+        n = int(rs.integers(1, 100_000))
+        x = rs.uniform(lo, hi, n)
+        data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
+        m0.set(rs.uniform(0.7, 1.1)); g.set(10 ** rs.uniform(-2.5, -0.5))
+        c0.set(rs.uniform(0.1, 2.0)); c1.set(rs.uniform(-0.1, 1.0))
+        n_bw.set(10 ** rs.uniform(0, 5)); n_poly.set(10 ** rs.uniform(0, 5))
+        d = (n_bw.value * (bw.eval((x,)) / bw_norm(region)) + n_poly.value * (poly.eval((x,)) / poly_norm(region)))
+        want = n_bw.value + n_poly.value - float(np.sum(np.log(d)))
+        with _lib.jit_mode(_lib.JIT_ALWAYS if case % 2 else _lib.JIT_OFF):   # NVRTC module / interpreter
+            got = hk.nll(model, data, ["x0"])
+        assert abs(got - want) <= 1e-10 * max(abs(want), 1.0), (case, got, want)
+    assert model._hk_sym          # the symbolic lowering served every call
