@@ -749,3 +749,51 @@ def test_nll_ragged_sizes_and_generic_models_vs_oracle(cuda, hk, oracle, n):
              ("gauss", 0.2 * n, 2.0, 1.5, oracle.gaussian_norm(2.0, 1.5, 0.0, 10.0)),
              ("exp", 0.5 * n, 3.0, oracle.exponential_norm(3.0, 0.0, 10.0))]
     assert hk.nll(three, store, ["x0"]) == pytest.approx(oracle.nll(x, comps), rel=1e-10, abs=1e-9)
+
+
+def test_random_decays_and_fused_chains_vs_oracle(cuda, hk, oracle):
+    """Randomised decays (2..8 daughters, random masses with thresholds of a
+    few percent to wide open, mothers at rest or boosted) and fused chains
+    (parent 2..6 daughters, sub-decay 2..4, random decaying daughter) against
+    the oracle: weights bit-exact, momenta within 1e-12 E, and the fused
+    chain's parent columns bit-identical to generate + decay_chain."""
+    import os
+    rs = np.random.default_rng(1717)
+    for case in range(int(os.environ.get("HK_TEST_RANDOM_CASES", "16"))):
+        n_d = int(rs.integers(2, 9))
+        masses = tuple(float(v) for v in rs.uniform(0.0, 1.0, n_d) * rs.choice([0.0, 1.0], n_d, p=[0.15, 0.85]))
+        M = sum(masses) + float(10 ** rs.uniform(-1.5, 0.7))
+        if rs.random() < 0.4:
+            p = tuple(float(v) for v in rs.normal(0, 2 * M, 3))
+            mother = (math.sqrt(M * M + sum(c * c for c in p)), *p)
+        else:
+            mother = (M, 0.0, 0.0, 0.0)
+        n = int(rs.integers(1, 3 * 4096 + 500))
+        key = (int(rs.integers(0, 1 << 62)), int(rs.integers(0, 5)))
+        spec = hk.DecaySpec(M, masses)
+        blk = _arr(hk.phsp_generate(spec, hk.FourVector(*mother), n, hk.RngKey(*key)))
+        ref = oracle.generate(masses, M, n, key[0], key[1], mother=mother, threads=4)
+        assert_block_parity(blk, np.stack(list(ref.values())), n_d, f"random decay {case}")
+        if n_d > 6:
+            continue
+        k = int(rs.integers(1, n_d + 1))
+        if masses[k - 1] <= 0.0:
+            continue
+        n_s = int(rs.integers(2, 5))
+        sub_m = tuple(float(v) for v in rs.uniform(0.0, masses[k - 1] / (n_s + 0.5), n_s))
+        sub = hk.DecaySpec(masses[k - 1], sub_m)
+        skey = (int(rs.integers(0, 1 << 62)), 1)
+        # the frame mass sqrt(E^2 - p^2) of a daughter boosted to gamma_k loses
+        # ~gamma_k^2 ulps to cancellation in the reference formula itself
+        # (phasespace.py:259-262), so ulp-level differences in the parent's
+        # momenta reach the sub-daughters as ~3e-16 gamma_k^2 E
+        # (profiles/r02_chain_gamma.txt): the 1e-12 E budget holds to gamma_k ~ 50
+        if float(np.max(ref[f"p{k}_e"])) > 40.0 * masses[k - 1]:
+            continue
+        fused = _arr(hk.phsp_generate_chain(spec, hk.FourVector(*mother), n, hk.RngKey(*key), k, sub,
+                                            hk.RngKey(*skey)))
+        two = _arr(hk.phsp_decay_chain(hk.phsp_generate(spec, hk.FourVector(*mother), n, hk.RngKey(*key)), k,
+                                       sub, hk.RngKey(*skey)))
+        _fused_vs_two_step(fused, two, k, n_s)
+        cref = oracle.decay_chain(ref, k, sub_m, masses[k - 1], skey[0], skey[1], threads=4)
+        assert_block_parity(fused, np.stack(list(cref.values())), n_d - 1 + n_s, f"random chain {case}")
