@@ -578,7 +578,8 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
       C4_generic  (1 GPU) FCN evals/s at 1e7 events for a Breit-Wigner +
                   polynomial model of closures (the density-program path)
       UNWEIGHT    phsp_unweight of the stored 1e8 block (accept flags + compaction)
-      TOYS        (1 GPU) generate_model_sample of the C4 model, 1e7 events"""
+      TOYS        (1 GPU) generate_model_sample of the C4 model, 1e7 events
+      SPLOT       (1 GPU) ratio_sums and splot_weights over the C4 data set"""
     from paper_1711_05683_b200.parallel import sharded_integrate
 
     spec, mother = hk.DecaySpec(M_B0, DAUGHTERS), hk.FourVector.at_rest(M_B0)
@@ -712,7 +713,34 @@ def other_configs(hk, torch, _lib, rank: int, world: int, dist) -> dict:
     if world == 1:
         out["C4_generic"] = fcn_generic(hk, torch)
         out["TOYS"] = toy_sample(hk, torch)
+        out["SPLOT"] = splot_pass(hk, torch)
     return out
+
+
+def splot_pass(hk, torch) -> dict:
+    """SURVEY 8f rank 2 on the C4 data set (1e7 events): the yield-stationarity
+    / sWeights-matrix accumulation (ratio_sums: K + K^2 sums per event, 8 B
+    read) and the per-event sWeights table (splot_weights: 8 B read, 8 K B
+    written), rows/s with CUDA events, HBM fraction of copy BW."""
+    import numpy as np
+
+    from paper_1711_05683_b200.fitting import ratio_sums
+    P = hk.Parameter
+    region = hk.BoundedRegion(((0.0, 10.0),))
+    g = hk.shape_gaussian(P("mean", 5.0), P("sigma", 0.5))
+    e = hk.shape_exponential(P("tau", 3.0))
+    model = hk.add_pdfs([P("n_sig", 4e6), P("n_bkg", 6e6)],
+                        [hk.make_pdf(g, hk.gaussian_norm(g), region), hk.make_pdf(e, hk.exponential_norm(e), region)])
+    data = hk.generate_model_sample(model, hk.RngKey(7, 2), poisson=False)
+    n = len(data)
+    peak = _peaks()["hbm_gbs"]
+    dt_sums = _timed(torch, lambda: ratio_sums(model, data, ["x0"]), 20)
+    V = np.eye(2)
+    dt_w = _timed(torch, lambda: hk.splot_weights(model, data, ["x0"], V), 20)
+    return {"what": "C4 data set (1e7): ratio_sums (yields / sWeights matrix) and splot_weights",
+            "ratio_sums_rows_per_s": n / dt_sums, "splot_weights_rows_per_s": n / dt_w,
+            "ratio_sums_frac_copy": 8 * n / dt_sums / 1e9 / peak,
+            "splot_weights_frac_copy": 24 * n / dt_w / 1e9 / peak}
 
 
 def toy_sample(hk, torch) -> dict:

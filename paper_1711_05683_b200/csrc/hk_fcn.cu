@@ -545,11 +545,8 @@ __global__ void __launch_bounds__(kBlock) k_yield(const double* __restrict__ x, 
     double acc[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) acc[w] = 0.0;
-#pragma unroll 1
-    for (int i = 0; i < kRowsPerThread; ++i) {
-      const int64_t r = ch * HK_CHUNK + i * kBlock + threadIdx.x;
-      if (r >= n) continue;
-      const double xv = __ldg(x + r);
+    // one row's contribution, in row order (the same sums whichever path)
+    const auto row = [&](double xv, int64_t r) {
       double p[K], d = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -572,6 +569,20 @@ __global__ void __launch_bounds__(kBlock) k_yield(const double* __restrict__ x, 
         acc[k] += p[k];
 #pragma unroll
         for (int j = 0; j < K; ++j) acc[K + k * K + j] += p[k] * p[j];
+      }
+    };
+    const int64_t r0 = ch * HK_CHUNK + threadIdx.x;
+    if (ch * HK_CHUNK + HK_CHUNK <= n) {  // full chunk: every row's load in flight first
+      double xv[kRowsPerThread];
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) xv[i] = __ldg(x + r0 + i * kBlock);
+#pragma unroll
+      for (int i = 0; i < kRowsPerThread; ++i) row(xv[i], r0 + i * kBlock);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < kRowsPerThread; ++i) {
+        const int64_t r = r0 + i * kBlock;
+        if (r < n) row(__ldg(x + r), r);
       }
     }
     block_sum_store<W>(acc, part + (int64_t)W * ch);
