@@ -5,13 +5,18 @@
 
 One step = generate EVENTS_PER_GPU events per GPU into HBM (13 fp64 SoA
 columns, 104 B/event), with the weight moments (sum w, sum w^2) fused into the
-same kernel, then the cross-GPU gather of the chunk partials (NCCL) and the
-deterministic fold -> weight sum / mean / variance.  Weak scaling: rank r
-generates global rows [r * EVENTS_PER_GPU, (r+1) * EVENTS_PER_GPU).
+same kernel, then the fold of each rank's partials into its 1024 super-chunk
+records, the cross-GPU gather of those records (NCCL) and the deterministic
+fold -> weight sum / mean / variance.  Weak scaling: rank r generates the
+global rows of its super-chunks (parallel.shard_range), ~EVENTS_PER_GPU each.
 
-Prints ONE JSON line on rank 0.  `--impl reference` times the reference
+Prints ONE JSON line on rank 0: the C2 headline with its roofline (copy and
+live write-only HBM), e2e through pinned host columns, clocks, the CPU
+baseline (the bit-exact C port, and the reference's own Python from
+baseline/_ref on C1-C5 and the FCN), the FCN (plain nll(), session, batched,
+fit), and the other configs.  `--impl reference` times the reference
 algorithm's CPU implementation (the bit-exact C oracle port, all host
-threads) on a bounded sample of the same workload.
+threads) on the same workload.
 """
 
 from __future__ import annotations
