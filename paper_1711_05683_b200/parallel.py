@@ -188,6 +188,8 @@ def shard_rows(store, rank: int, world: int):
 
 
 _PART = 3 + _lib.HK_FCN_MAX_OBS   # host-path record: logsum, global row (-1), kind, payload
+_OFFSET_SET: dict = {}             # id(FCN workspace) -> (its pointer, the row offset written into [6])
+_GATHERED: dict = {}               # (device, stream, world, group) -> the all-gather target of the FCN records
 
 
 def combine_nll_parts(parts, expected_total: float) -> float:
@@ -238,11 +240,18 @@ def sharded_nll(model, shard, observable_columns, row_offset: int, group=None,
     none = np.array([-1], dtype=np.int64).view(np.float64)[0]
     if len(shard):
         work = fitting.nll_event_launch(model, shard, observable_columns)
-        work[6] = float(row_offset)
+        # [6] = the shard's first global row: the kernel never writes it, so it
+        # is set once per workspace and offset (a device write costs a launch)
+        if _OFFSET_SET.get(id(work)) != (work.data_ptr(), row_offset):
+            work[6] = float(row_offset)
+            _OFFSET_SET[id(work)] = (work.data_ptr(), row_offset)
         rec = work[:8]
     else:
         rec = torch.from_numpy(np.array([0.0, none, 0, 0, 0, none, float(row_offset), 0.0])).to(_lib.device())
-    gathered = torch.empty(world * 8, dtype=torch.float64, device=rec.device)
+    key = (rec.device.index, _lib.stream_ptr(), world, id(group))
+    gathered = _GATHERED.get(key)
+    if gathered is None:   # the gather target is reused: stream-ordered, read by the combine kernel
+        gathered = _GATHERED[key] = torch.empty(world * 8, dtype=torch.float64, device=rec.device)
     dist.all_gather_into_tensor(gathered, rec, group=group)
     logsum = _lib.ctypes.c_double()
     bad, zero = _lib.ctypes.c_uint64(), _lib.ctypes.c_uint64()
