@@ -309,6 +309,27 @@ __device__ __forceinline__ void boost_rest(const Frame& f, double m, double& e, 
   pz = e * f.bz;
 }
 
+// Lorentz boost into the lab of a frame with four-momentum (fe, P) and FIXED
+// mass m (im = 1/m, rem = 1/(fe + m)): with beta = P/fe and gamma = fe/m,
+//   E' = (fe E + P.p) / m,   p' = p + P ((P.p) / (fe + m) + E) / m,
+// the same transformation as _boost (phasespace.py:74-81) with gamma^2/(gamma+1)
+// (beta.p) beta rewritten through m -- 10 FP64 instructions per daughter and
+// one reciprocal per frame instead of make_frame_fast's three.  Used by the
+// fused chain when the host has proved the frame mass is the decay's (see
+// hk_phsp_generate_chain); rounding differs from _boost's by a few ulp * E.
+struct MFrame {
+  double e, px, py, pz, im, rem;
+};
+
+__device__ __forceinline__ void boost_m(const MFrame& f, double& e, double& px, double& py, double& pz) {
+  const double s = fma(f.px, px, fma(f.py, py, f.pz * pz));
+  const double c = fma(s, f.rem, e) * f.im;
+  e = fma(f.e, e, s) * f.im;
+  px = fma(c, f.px, px);
+  py = fma(c, f.py, py);
+  pz = fma(c, f.pz, pz);
+}
+
 // Branch-free correctly rounded sqrt for positive normal x whose result is
 // normal: MUFU rsqrt seed, two Newton steps to y ~ 1/sqrt(x) (error far below
 // 2^-53), then Markstein's residual correction s + (x - s^2) y/2.  Verified
@@ -402,9 +423,16 @@ __device__ __forceinline__ void cswap(uint64_t& a, uint64_t& b) {
 // bit-identical): 1/(2M) of the last breakup (M = inv[N-1] is fixed by the
 // decay) and the first cluster frame's gamma multiplier: 1/inv[0], or +inf
 // when inv[0] = m1 = 0 (so fe * gmul0 is IEEE fe / +0).
+// HK_GEN_MBOOST: the generator's cluster boosts through the cluster's exact
+// mass (boost_m) and daughter 1's first boost as the cluster itself
+#ifndef HK_GEN_MBOOST
+#define HK_GEN_MBOOST 1
+#endif
+
 struct RestHoist {
   double rcp_2m_last;
   double gmul0;  // make_frame_fast_r's gamma multiplier of the first cluster frame
+  bool m0_zero;  // daughter 1 massless: its first boost is the reference's NaN
 };
 
 template <int N>
@@ -412,6 +440,7 @@ __device__ __forceinline__ RestHoist rest_hoist(const hk_decay_t& d) {
   RestHoist h;
   h.rcp_2m_last = fast_rcp(2.0 * (d.T + d.csum[N - 1]));
   h.gmul0 = d.csum[0] == 0.0 ? __longlong_as_double(0x7ff0000000000000ll) : fast_rcp(d.csum[0]);
+  h.m0_zero = d.csum[0] == 0.0;
   return h;
 }
 
@@ -459,6 +488,36 @@ __device__ __forceinline__ double rest_event_bits(const hk_decay_t& d, uint64_t 
     const double clm = inv[k - 1];
     const double cle = fast_sqrt(q * q + clm * clm);
     const double clx = q * nx, cly = q * ny, clz = q * nz;
+#if HK_GEN_MBOOST
+    if (k == 1) {
+      // daughter 1 starts at rest and is boosted by the cluster it alone makes
+      // up (mass inv_0 = m_1): the result is the cluster's own four-momentum,
+      // (cle, q n), within a few ulp of the reference's rounding.  m_1 = 0
+      // gives the reference's gamma = inf -> NaN daughter (hoisted flag).
+      if (h.m0_zero) {
+        const double nan = __longlong_as_double(0x7ff8000000000000ll);
+        p[0] = nan;
+        p[1] = nan;
+        p[2] = nan;
+        p[3] = nan;
+      } else {
+        p[0] = cle;
+        p[1] = clx;
+        p[2] = cly;
+        p[3] = clz;
+      }
+    } else if (__double2hiint(clm) > 0) {  // clm > 0 (clm >= 0 here), tested on the integer pipe
+      // the cluster's mass is inv_{k-1} exactly: the fixed-mass boost (one
+      // reciprocal per frame for 1/m and one for 1/(E + m), 10 FP64 per daughter)
+      const MFrame f{cle, clx, cly, clz, fast_rcp(clm), fast_rcp(cle + clm)};
+#pragma unroll
+      for (int j = 0; j < k; ++j) boost_m(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+    } else {  // a massless cluster: the reference's gamma = inf arithmetic, exactly
+      const Frame f = make_frame_fast(cle, clx, cly, clz, clm);
+#pragma unroll
+      for (int j = 0; j < k; ++j) boost_fma(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+    }
+#else
     const Frame f = k == 1 ? make_frame_fast_r(cle, clx, cly, clz, h.gmul0)
                            : make_frame_fast(cle, clx, cly, clz, clm);
     if (k == 1) {
@@ -467,6 +526,7 @@ __device__ __forceinline__ double rest_event_bits(const hk_decay_t& d, uint64_t 
 #pragma unroll
       for (int j = 0; j < k; ++j) boost_fma(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
     }
+#endif
     p[4 * k + 0] = fast_sqrt(q * q + d.masses[k] * d.masses[k]);
     p[4 * k + 1] = -clx;
     p[4 * k + 2] = -cly;
@@ -516,27 +576,6 @@ __device__ __forceinline__ TwoBody two_body_consts(const hk_decay_t& d) {
   t.m0 = d.masses[0];
   t.e1 = cle;
   return t;
-}
-
-// Lorentz boost into the lab of a frame with four-momentum (fe, P) and FIXED
-// mass m (im = 1/m, rem = 1/(fe + m)): with beta = P/fe and gamma = fe/m,
-//   E' = (fe E + P.p) / m,   p' = p + P ((P.p) / (fe + m) + E) / m,
-// the same transformation as _boost (phasespace.py:74-81) with gamma^2/(gamma+1)
-// (beta.p) beta rewritten through m -- 10 FP64 instructions per daughter and
-// one reciprocal per frame instead of make_frame_fast's three.  Used by the
-// fused chain when the host has proved the frame mass is the decay's (see
-// hk_phsp_generate_chain); rounding differs from _boost's by a few ulp * E.
-struct MFrame {
-  double e, px, py, pz, im, rem;
-};
-
-__device__ __forceinline__ void boost_m(const MFrame& f, double& e, double& px, double& py, double& pz) {
-  const double s = fma(f.px, px, fma(f.py, py, f.pz * pz));
-  const double c = fma(s, f.rem, e) * f.im;
-  e = fma(f.e, e, s) * f.im;
-  px = fma(c, f.px, px);
-  py = fma(c, f.py, py);
-  pz = fma(c, f.pz, pz);
 }
 
 // Two-body decay in the fixed frame f: daughters (e1, q n) and (e2, -q n) in
