@@ -321,6 +321,15 @@ struct MFrame {
   double e, px, py, pz, im, rem;
 };
 
+// boost_m with the dot product P.p = s supplied by the caller
+__device__ __forceinline__ void boost_m_s(const MFrame& f, double s, double& e, double& px, double& py, double& pz) {
+  const double c = fma(s, f.rem, e) * f.im;
+  e = fma(f.e, e, s) * f.im;
+  px = fma(c, f.px, px);
+  py = fma(c, f.py, py);
+  pz = fma(c, f.pz, pz);
+}
+
 __device__ __forceinline__ void boost_m(const MFrame& f, double& e, double& px, double& py, double& pz) {
   const double s = fma(f.px, px, fma(f.py, py, f.pz * pz));
   const double c = fma(s, f.rem, e) * f.im;
@@ -510,8 +519,17 @@ __device__ __forceinline__ double rest_event_bits(const hk_decay_t& d, uint64_t 
       // the cluster's mass is inv_{k-1} exactly: the fixed-mass boost (one
       // reciprocal per frame for 1/m and one for 1/(E + m), 10 FP64 per daughter)
       const MFrame f{cle, clx, cly, clz, fast_rcp(clm), fast_rcp(cle + clm)};
+      if (k == 2 && !h.m0_zero) {
+        // daughters 1 and 2 are back to back in the cluster they came from
+        // (momenta q n and -q n): P.p is computed once, exactly negated (a
+        // massless daughter 1 is the reference's NaN and must not leak into 2)
+        const double s0 = fma(f.px, p[1], fma(f.py, p[2], f.pz * p[3]));
+        boost_m_s(f, s0, p[0], p[1], p[2], p[3]);
+        boost_m_s(f, -s0, p[4], p[5], p[6], p[7]);
+      } else {
 #pragma unroll
-      for (int j = 0; j < k; ++j) boost_m(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+        for (int j = 0; j < k; ++j) boost_m(f, p[4 * j], p[4 * j + 1], p[4 * j + 2], p[4 * j + 3]);
+      }
     } else {  // a massless cluster: the reference's gamma = inf arithmetic, exactly
       const Frame f = make_frame_fast(cle, clx, cly, clz, clm);
 #pragma unroll
