@@ -396,7 +396,9 @@ int hk_nll_program_eval(const double* const* d_obs, int64_t n, const hk_density_
 int hk_nll_combine(const double* d_gathered, int32_t world, double* h_logsum, uint64_t* h_first_bad,
                    uint64_t* h_first_div0, void* stream);
 
-/* Yield-stationarity / sPlot sums for an hk_density_t (any shape, K <= 8):
+/* Yield-stationarity / sPlot sums for an hk_density_t (any shape, K <= 8 per pass; the host
+ * covers more components with passes whose slot 0 is the density at yield 1, fitting.py
+ * _ratio_sums_passes):
  * per chunk K values sum_e r_k and K*K values sum_e r_k r_j, r_k = pdf_k / d,
  * d = sum_k N_k pdf_k; d_first_bad[0]: d not > 0; [1]: d not > 0 or
  * non-finite; [2]: first zero divisor (all initialised to HK_NO_BAD_ROW). */

@@ -61,6 +61,56 @@ def splot_matrix(model: ExtendedModel, store: ColumnStore, observable_columns: S
     return np.linalg.inv(vinv)
 
 
+def _weights_passes(model: ExtendedModel, obs, n: int, V: np.ndarray, cols: list) -> list:
+    """sWeights for more species than one pass pins: per block of up to
+    HK_MAX_COMPONENTS - 1 species s (fewer when the numerators would exceed a
+    program's HK_MAX_PROGRAM ops), a pass whose slot 0 is the density and
+    whose further slots are the numerators sum_j V[s, j] pdf_j, accumulated
+    left to right as hk_splot_weights_program does (splot.py:114); an
+    identity V' then writes numerator / density.  Slot 0's output goes to a
+    scratch column.  Returns the first-bad rows of the first pass."""
+    from .fitting import _lower_pass
+    k = len(model.components)
+    B = _lib.HK_MAX_COMPONENTS - 1
+    scratch = _lib.empty(n)
+    flags = None
+    a = 0
+    while a < k:
+        species = list(range(a, min(a + B, k)))
+
+        def numerators(pdfs, species=species):
+            out = []
+            for s in species:
+                num = None
+                for j in range(k):
+                    term = ("mul", pdfs[j], ("const", float(V[s, j])))
+                    num = term if num is None else ("add", num, term)
+                out.append(num)
+            return out
+
+        try:
+            dm = _lower_pass(model, numerators)
+        except NotImplementedError:
+            if B == 1:                  # one numerator does not fit a program
+                raise
+            B //= 2                     # fewer numerators per pass (HK_MAX_PROGRAM ops)
+            continue
+        a += len(species)
+        Kp = dm.n_comp
+        ident = np.zeros((Kp, Kp))
+        ident[1:, 1:] = np.eye(Kp - 1)
+        vflat = np.ascontiguousarray(ident.ravel())
+        vptr = vflat.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_double))
+        bad = _lib.bad_cells(3)
+        _lib.check(_lib.lib().hk_splot_weights_program(_lib.ptr_array(obs), n, dm, vptr,
+                                                       _lib.ptr_array([scratch] + [cols[s] for s in species]),
+                                                       _lib.ptr(bad), _lib.stream_ptr()),
+                   "hk_splot_weights_program")
+        got = _lib.read_bad(bad)
+        flags = got if flags is None else flags
+    return flags
+
+
 def splot_weights(model: ExtendedModel, store: ColumnStore, observable_columns: Sequence[str],
                   V: np.ndarray, workers: int | None = 1) -> ColumnStore:
     """Per-event sWeights table, columns sw_<species> (splot.py:90-117), on the GPU."""
@@ -73,7 +123,9 @@ def splot_weights(model: ExtendedModel, store: ColumnStore, observable_columns: 
     cols = [_lib.empty(n) for _ in range(k)]
     vflat = np.ascontiguousarray(V.ravel())
     vptr = vflat.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_double))
-    if _closed_form(model) and k <= 4:
+    if k > _lib.HK_MAX_COMPONENTS:
+        flags = _weights_passes(model, obs, n, V, cols)
+    elif _closed_form(model) and k <= 4:
         bad = _lib.bad_cells(1)
         _lib.check(_lib.lib().hk_splot_weights(_lib.ptr(obs[0]), n, lower_model(model), vptr,
                                                _lib.ptr_array(cols), _lib.ptr(bad), _lib.stream_ptr()),

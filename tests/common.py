@@ -34,8 +34,9 @@ def assert_block_parity(got: np.ndarray, ref: np.ndarray, n_daughters: int, what
             assert np.all(d <= lim), f"{what}: daughter {j + 1} comp {c} max |d|/E {np.max(d / lim) * 1e-12}"
 
 
-def run_program_numpy(prog, cols: list[np.ndarray]) -> tuple[np.ndarray, np.ndarray]:
-    """Vectorised emulation of hk::run_program (csrc/hk_device.cuh)."""
+def run_program_numpy(prog, cols: list[np.ndarray], want_slots: bool = False):
+    """Vectorised emulation of hk::run_program (csrc/hk_device.cuh):
+    (result, zero-divisor mask[, the final slot values])."""
     from paper_1711_05683_b200 import _lib as L
 
     n = len(cols[0])
@@ -83,7 +84,7 @@ def run_program_numpy(prog, cols: list[np.ndarray]) -> tuple[np.ndarray, np.ndar
             else:
                 raise ValueError(op)
             r[prog.dst[i]] = v
-    return r[prog.result], div0
+    return (r[prog.result], div0, r) if want_slots else (r[prog.result], div0)
 
 
 def m12sq_builder(cols):

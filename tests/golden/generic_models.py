@@ -6,7 +6,8 @@ tests/test_fcn_generic_gpu.py.
 * g1 -- Breit-Wigner + linear polynomial (closures, closed-form norms), 1-D;
 * g2 -- observable arity 2: Gaussian(x) * exponential(y) through
   compose/coordinate/combine, plus a 2-D closure background;
-* g6 -- six components (four Gaussians, an exponential, a flat closure).
+* g6 -- six components (four Gaussians, an exponential, a flat closure);
+* g12 -- twelve components (ten Gaussians, an exponential, a flat closure).
 """
 
 from __future__ import annotations
@@ -72,7 +73,26 @@ def generic_models(hk_mod, np_mod, values):
     comps.append(hk_mod.make_pdf(flat, lambda r: 10.0, reg6))
     ys.append(P("y5", v["y5"]))
     out["g6"] = hk_mod.add_pdfs(ys, comps)
+    # G12: twelve components (ten Gaussians, an exponential, a flat closure):
+    # above the device's pinned-slot limit (HK_MAX_COMPONENTS = 8), so the
+    # ratio sums and sWeights run in passes
+    comps, ys = [], []
+    for i in range(10):
+        mu, s = G12_MEANS[i], 0.2 + 0.03 * i
+        gs = hk_mod.shape_gaussian(P(f"m12_{i}", v.get(f"m12_{i}", mu)), P(f"s12_{i}", v.get(f"s12_{i}", s)))
+        comps.append(hk_mod.make_pdf(gs, hk_mod.gaussian_norm(gs), reg6))
+        ys.append(P(f"z{i}", v.get(f"z{i}", 800.0 + 40.0 * i)))
+    ex12 = hk_mod.shape_exponential(P("tau12", v.get("tau12", 2.5)))
+    comps.append(hk_mod.make_pdf(ex12, hk_mod.exponential_norm(ex12), reg6))
+    ys.append(P("z10", v.get("z10", 2000.0)))
+    flat12 = hk_mod.wrap_closure(lambda x, p: np_mod.ones_like(x[0]) * 1.0, [])
+    comps.append(hk_mod.make_pdf(flat12, lambda r: 10.0, reg6))
+    ys.append(P("z11", v.get("z11", 1200.0)))
+    out["g12"] = hk_mod.add_pdfs(ys, comps)
     return out
+
+
+G12_MEANS = [0.5 + 0.95 * i for i in range(10)]
 
 
 GENERIC_POINTS = [
@@ -82,5 +102,5 @@ GENERIC_POINTS = [
     {"m0": 0.90, "g": 0.052, "c0": 1.1, "c1": 0.3, "n_bw": 3100.0, "n_poly": 8800.0,
      "mx": 5.2, "sx": 0.7, "ty": 2.2, "a2": 0.08, "n_sig2": 4200.0, "n_bkg2": 7700.0,
      "y0": 1400.0, "y1": 2600.0, "y2": 1900.0, "y3": 1900.0, "y4": 3100.0, "y5": 1400.0, "tau6": 3.3,
-     "mu1": 4.1, "s2": 0.45},
+     "mu1": 4.1, "s2": 0.45, "z3": 950.0, "m12_4": 4.3, "s12_7": 0.35, "tau12": 2.8},
 ]

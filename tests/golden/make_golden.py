@@ -32,7 +32,7 @@ from hepkit.fitting import generate_model_sample  # noqa: E402
 import toymodel  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from generic_models import GENERIC_POINTS, generic_models  # noqa: E402
+from generic_models import G12_MEANS, GENERIC_POINTS, generic_models  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -159,7 +159,14 @@ def add_generic_models(arrays, scalars) -> None:
     s1 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g1_x"]])
     s2 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0", "x1"), [arrays["g2_x"], arrays["g2_y"]])
     s6 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g6_x"]])
-    out = {"points": GENERIC_POINTS, "g1": [], "g2": [], "g6": [], "g6_yields": []}
+    # G12 data on [0, 10] (its own generator: the arrays above stay as they were)
+    r12 = np.random.default_rng(20261019)
+    n12 = 2 * 4096 + 29
+    arrays["g12_x"] = np.clip(np.concatenate([r12.normal(mu, 0.3, n12 // 12) for mu in G12_MEANS]
+                                             + [r12.exponential(2.5, n12 // 12),
+                                                r12.uniform(0, 10, n12 - 11 * (n12 // 12))]), 0.01, 9.99)
+    s12 = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [arrays["g12_x"]])
+    out = {"points": GENERIC_POINTS, "g1": [], "g2": [], "g6": [], "g6_yields": [], "g12": [], "g12_yields": []}
     from hepkit.fitting import _yield_stationarity
     for pt in GENERIC_POINTS:
         ms = generic_models(hk, np, pt)
@@ -168,6 +175,15 @@ def add_generic_models(arrays, scalars) -> None:
         out["g6"].append(hk.nll(ms["g6"], s6, ["x0"]))
         g, A = _yield_stationarity(ms["g6"], s6, ["x0"], 1)
         out["g6_yields"].append({"g": g.tolist(), "A": A.tolist()})
+        out["g12"].append(hk.nll(ms["g12"], s12, ["x0"]))
+        g, A = _yield_stationarity(ms["g12"], s12, ["x0"], 1)
+        out["g12_yields"].append({"g": g.tolist(), "A": A.tolist()})
+    # sWeights of G12 at the first point with V = A^-1 (splot_weights takes any V)
+    m12 = generic_models(hk, np, GENERIC_POINTS[0])["g12"]
+    V12 = np.linalg.inv(np.asarray(out["g12_yields"][0]["A"]))
+    arrays["g12_V"] = V12
+    sw = hk.splot_weights(m12, s12, ["x0"], V12)
+    arrays["g12_sw"] = np.stack([np.asarray(sw.column(n)) for n in sw.schema.names])
     scalars["generic"] = out
 
 def main() -> None:

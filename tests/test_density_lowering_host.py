@@ -87,3 +87,32 @@ def test_symbolic_path_raises_the_shape_errors(hk):
     s.value = -1.0
     with pytest.raises(EvaluationError, match="sigma must be positive, got -1.0"):
         fitting.lower_density(model)
+
+
+def test_many_components_lowering(hk):
+    """Twelve components (above HK_MAX_COMPONENTS): the FCN's density has one
+    pinned slot, the density itself with yield 1; a ratio / sWeight pass
+    (_lower_pass) pins the density (yield 1) and the picked expressions
+    (yield 0), so the kernels' d = sum_k N_k p_k is the density."""
+    from paper_1711_05683_b200 import _lib, fitting
+    rs = np.random.default_rng(5)
+    model = generic_models(hk, np, GENERIC_POINTS[0])["g12"]
+    K = len(model.components)
+    assert K > _lib.HK_MAX_COMPONENTS
+    x = [rs.uniform(0.0, 10.0, 3000)]
+    dm = fitting.lower_density(model)
+    assert dm.n_comp == 1 and dm.yield_[0] == 1.0
+    dens, _, slots = run_program_numpy(dm.program, x, want_slots=True)
+    assert np.array_equal(slots[dm.pdf_slot[0]], dens)
+    sel = [0, 5, 11]
+    pm = fitting._lower_pass(model, lambda pdfs: [pdfs[k] for k in sel])
+    assert pm.n_comp == 1 + len(sel)
+    assert list(pm.yield_[:pm.n_comp]) == [1.0, 0.0, 0.0, 0.0]
+    d2, _, s2 = run_program_numpy(pm.program, x, want_slots=True)
+    assert np.array_equal(d2, dens) and np.array_equal(s2[pm.pdf_slot[0]], dens)
+    with np.errstate(all="ignore"):
+        total = sum(float(y.value) * s2[pm.pdf_slot[1 + sel.index(k)]] for k, (y, _) in
+                    enumerate(model.components) if k in sel)
+    assert np.all(total < dens)
+    with pytest.raises(ValueError):
+        fitting._lower_pass(model, lambda pdfs: pdfs[:_lib.HK_MAX_COMPONENTS])
