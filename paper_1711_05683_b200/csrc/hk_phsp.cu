@@ -533,6 +533,10 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const long long* in, int64
   if (t == 1023) *total = sm[1023];
 }
 
+#ifndef HK_COMPACT_GROUP
+#define HK_COMPACT_GROUP 16  // columns per load group in k_compact (0: one column at a time)
+#endif
+
 struct CompactArgs {
   const double* in[kMaxCols];
   double* out[kMaxCols];
@@ -597,8 +601,25 @@ __global__ void __launch_bounds__(kBlock) k_compact(const __grid_constant__ Comp
       if (f) {
         const int64_t dst = base + s_pre[i * kWarps + warp] + __popc(m & lt);
         const int64_t r = c0 + i * kBlock;
+#if HK_COMPACT_GROUP > 0
+        // a group of columns loaded before any is stored: the outputs may
+        // alias the inputs as far as the compiler knows, so a load-store
+        // loop would wait one memory latency per column
+        for (int g = 0; g < a.n_cols; g += HK_COMPACT_GROUP) {
+          double v[HK_COMPACT_GROUP];
+#pragma unroll
+          for (int k = 0; k < HK_COMPACT_GROUP; ++k) {
+            const int col = g + k;
+            if (col < a.n_cols) v[k] = col == a.weight_col ? 1.0 : __ldcs(a.in[col] + r);
+          }
+#pragma unroll
+          for (int k = 0; k < HK_COMPACT_GROUP; ++k)
+            if (g + k < a.n_cols) a.out[g + k][dst] = v[k];
+        }
+#else
         for (int col = 0; col < a.n_cols; ++col)
           a.out[col][dst] = col == a.weight_col ? 1.0 : __ldcs(a.in[col] + r);
+#endif
       }
     }
     __syncthreads();
