@@ -79,6 +79,7 @@ def _fp64_roofline(kernel: str, events_per_s_per_gpu: float, note: str = "") -> 
     inst = events_per_s_per_gpu * k["dp_inst_per_event"]
     return {"bound": "fp64", "achieved": inst * 1e-12, "peak": pk["dp_inst_per_s"] * 1e-12,
             "unit": "T DP inst/s", "frac": inst / pk["dp_inst_per_s"], "dp_inst_per_event": k["dp_inst_per_event"],
+            "frac_ncu_one_launch": k.get("dp_inst_frac_of_peak_ncu"),
             **({"note": note} if note else {})}
 
 
@@ -529,6 +530,12 @@ def fcn_minimiser_paths(hk, torch, model, data, points, pars, evals: int) -> dic
     for _ in range(10):
         nll_many(model, data, ["x0"], pts)
     res["batched51_evals_per_s"] = 51 * 10 / (time.perf_counter() - t0)
+    # the batched kernel's FP64 roofline at the API rate (host clock: launch,
+    # fold and result read included); the 51 points run as 26 pairs (52)
+    rf = _fp64_roofline("k_nll_many", res["batched51_evals_per_s"] / 51 * 52 * len(data),
+                        note="event-points/s at the nll_many API rate, 51 points padded to 52")
+    if rf:
+        res["batched51_roofline"] = rf
     saved = ps.values()
     ps["mean"].set(4.8); ps["sigma"].set(0.6); ps["tau"].set(2.6)
     t0 = time.perf_counter()

@@ -22,6 +22,7 @@ EVENTS = {  # events per launch in tools/prof_kernels.py
     "hk_jit_integrate": 100_000_000,
     "k_generate_chain<": 50_000_000,
     "k_nll_fused<": 10_000_000,
+    "k_nll_many<": 10_000_000 * 52,   # event-points: 52 parameter points per launch
 }
 
 

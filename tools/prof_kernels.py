@@ -3,7 +3,7 @@
     python tools/prof_kernels.py [--n 100000000]
 
 Order of launches (for -k/-s/-c selection): k_generate x3, k_integrate x2,
-k_generate_chain x2, k_nll x3.
+k_generate_chain x2, k_nll x3, k_nll_many x2 (52 points each).
 """
 
 from __future__ import annotations
@@ -60,6 +60,14 @@ def main() -> None:
     data = hk.ColumnStore.from_columns(hk.ColumnSchema.real64("x0"), [x])
     for _ in range(3):
         v = hk.nll(model, data, ["x0"])
+    # the batched multi-point pass: 52 points (26 groups of 2) in one launch
+    from paper_1711_05683_b200.fitting import nll_many
+    base = model.param_set().values()
+    names = model.param_set().names
+    pts = [tuple(b * (1.0 + 1e-4 * (k + 1)) if nm in ("mean", "sigma", "tau") else b for nm, b in zip(names, base))
+           for k in range(52)]
+    for _ in range(2):
+        nll_many(model, data, ["x0"], pts)
     torch.cuda.synchronize()
     print(f"ok <m12^2>={r.value:.12g} nll={v:.12g}")
 
