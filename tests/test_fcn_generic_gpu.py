@@ -521,3 +521,38 @@ def test_nll_random_closure_models_vs_numpy(cuda, hk):
             got = hk.nll(model, data, ["x0"])
         assert abs(got - want) <= 1e-10 * max(abs(want), 1.0), (case, got, want)
     assert model._hk_sym          # the symbolic lowering served every call
+
+
+def test_many_components_first_bad_event(cuda, hk, golden):
+    """Twelve components with a negative yield: nll, the yield sums (the
+    density-only flag pass) and sWeights name the first event whose density
+    is not positive -- the row a numpy restatement of the density finds
+    (fitting.py:200-205, :416-418, splot.py:114)."""
+    import math
+
+    from paper_1711_05683_b200.fitting import _yield_stationarity
+    from tests.golden.generic_models import G12_MEANS
+    arrays, _ = golden
+    store, cols = _stores(hk, arrays)["g12"]
+    x = arrays["g12_x"]
+    model = generic_models(hk, np, dict(GENERIC_POINTS[0], z5=-2.0e5))["g12"]
+    # numpy restatement of sum_k N_k shape_k(x) / norm_k on [0, 10]
+    dens = np.zeros_like(x)
+    for i in range(10):
+        mu, s, y = G12_MEANS[i], 0.2 + 0.03 * i, (-2.0e5 if i == 5 else 800.0 + 40.0 * i)
+        nm = s * math.sqrt(2.0 * math.pi) * 0.5 * (math.erf((10.0 - mu) / (s * math.sqrt(2.0)))
+                                                   - math.erf((0.0 - mu) / (s * math.sqrt(2.0))))
+        dens += y * np.exp(-0.5 * ((x - mu) / s) ** 2) / nm
+    tau = 2.5
+    dens += 2000.0 * np.exp(-x / tau) / (tau * (1.0 - math.exp(-10.0 / tau)))
+    dens += 1200.0 * np.ones_like(x) / 10.0
+    bad = np.flatnonzero(~(dens > 0))
+    assert bad.size and bad[0] > 0
+    j = int(bad[0])
+    assert abs(dens[j]) > 1e-6 * np.max(np.abs(dens))     # not a rounding-level crossing
+    with pytest.raises(ValueError, match=rf"is not positive at event {j}$"):
+        hk.nll(model, store, cols)
+    with pytest.raises(ValueError, match=rf"model density is not positive at event {j}$"):
+        _yield_stationarity(model, store, cols)
+    with pytest.raises(ValueError, match=rf"is not positive at event {j}$"):
+        hk.splot_weights(model, store, cols, np.eye(12))
